@@ -1,0 +1,167 @@
+/* aaa.h — C ABI of the B200-native AAA-Gaussians forward renderer (arxiv 2504.12811).
+ *
+ * The library renders a set of 3D Gaussians (mean mu, scale s, rotation q, opacity o,
+ * SH colour, stored training frequency v_train) from a pinhole
+ * camera (V, P, M_vp, f) with the paper's four stages:
+ *   1. per-Gaussian preprocess: adaptive 3D smoothing filter and perpendicular amplitude
+ *      (Eq. 6-13), SH colour, view-space bounding (Eq. 14-17),
+ *      camera-inside discard, whole-view-frustum cull;
+ *   2. 3D tile-frustum culling (Eq. 18) and (tile, depth) key emission;
+ *   3. a global onesweep radix sort of the keys and per-tile ranges;
+ *   4. per-tile hierarchical re-sort with per-pixel 3D evaluation at the maximum-response
+ *      point (Eq. 4-5), front-to-back blending with early termination.
+ * All of it runs in hand-written sm_100a CUDA kernels; nothing here falls back to the CPU.
+ *
+ * Conventions: view space +z forward, y down; pixel (i, j) has its
+ * centre at (i + 0.5, j + 0.5); x_pix = fx X/Z + cx. Quaternions are (w, x, y, z).
+ * Inputs are post-activation (scales > 0, opacity in (0,1)).
+ *
+ * Threading: one context per host thread; calls on one context are not thread-safe.
+ * Errors: every call returns aaa_status; aaa_last_error() gives a per-context message that
+ * stays valid until the next call on that context. Asynchronous CUDA errors surface at the
+ * next synchronising call as AAA_ERR_CUDA.
+ * Determinism: identical inputs give bit-identical images, keys and values.
+ */
+#ifndef AAA_H_
+#define AAA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AAA_OK = 0,
+    AAA_ERR_INVALID_ARG = -1,      /* null pointer, bad camera/config value, bad sizes      */
+    AAA_ERR_INVALID_GAUSSIAN = -2, /* load-time validation failed; see first_bad   */
+    AAA_ERR_CUDA = -3,             /* CUDA runtime error (message from cudaGetErrorString) */
+    AAA_ERR_OOM = -4,              /* device allocation failed                              */
+    AAA_ERR_STATE = -5             /* call out of order (e.g. render before load/camera)    */
+} aaa_status;
+
+typedef struct aaa_ctx aaa_ctx; /* opaque; owns all device state of one renderer */
+
+/* Pinhole camera. world_to_view: row-major 4x4 rigid transform whose upper
+ * 3x3 is a rotation (det +1) and whose last row is (0,0,0,1). Requirements: width, height
+ * in [1, 65535]; fx, fy > 0; near_z > 0 (default 0.01, reading 7). */
+typedef struct {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float world_to_view[16];
+    float near_z;
+} aaa_camera;
+
+/* Render configuration. Defaults from aaa_default_config():
+ *   k = 0.3; tau_mode 0: tau = 2 ln(255 o A) per Gaussian (reading 1), tau_mode 1:
+ *   tau = min(tau_fixed, 2 ln(255 o A)) with tau_fixed = 9; alpha_max = 0.99 (reading 2);
+ *   T_eps = 1e-4 (reading 3); background black; window_k = 16 (per-pixel re-sort window,
+ *   16 or 32); flags = 0. */
+typedef struct {
+    float k;
+    int32_t tau_mode;
+    float tau_fixed;
+    float alpha_max;
+    float T_eps;
+    float background[3];
+    int32_t window_k;
+    uint32_t flags;
+} aaa_config;
+
+/* Scene arrays, structure-of-arrays, float32:
+ *   means N x 3, scales N x 3 (standard deviations, > 0), quats N x 4 (w,x,y,z, nonzero),
+ *   opacities N (in (0,1)), sh N x (deg+1)^2 x 3 (coefficient-major, channel-minor),
+ *   v_train N (> 0 or +inf).
+ * device_ptrs = 1: the pointers are CUDA device memory on the context's device; 0: host. */
+typedef struct {
+    const float *means, *scales, *quats, *opacities, *sh, *v_train;
+    int64_t n;
+    int32_t sh_degree; /* 0..3 */
+    int32_t device_ptrs;
+} aaa_gaussians;
+
+/* Counters of the last rendered view: N loaded, V visible after preprocessing,
+ * C candidate (Gaussian, tile) pairs from the bounds, P pairs kept by 3D tile culling,
+ * tiles whose per-pixel window overflowed (re-rendered by the quarter-tile K = 128 kernel),
+ * quarters that overflowed again (re-rendered by the exact collect-and-sort kernel), pixels
+ * whose contributions exceeded that kernel's capacity (0 unless the image is wrong),
+ * Gaussians taking the near-plane-crossing cull path. ms[]: per-stage device times when
+ * AAA_FLAG_TIMING is set (0 preprocess, 1 scan, 2 cull/emit, 3 sort, 4 ranges, 5 raster,
+ * 6 fallback, 7 total). */
+typedef struct {
+    int64_t n, visible, candidates, pairs, overflow_tiles, overflow_quarters, unresolved_pixels, crossing;
+    float ms[8];
+} aaa_stats;
+
+enum { AAA_FLAG_TIMING = 1u, AAA_FLAG_NO_TILE_CULL = 2u, AAA_FLAG_FORCE_FALLBACK = 4u };
+
+/* what for aaa_debug_copy (parity tests only; synchronises) */
+enum {
+    AAA_DBG_GAUSS = 0,  /* N x AAA_DBG_GAUSS_FIELDS float64 per-Gaussian preprocess record  */
+    AAA_DBG_KEYS = 1,   /* P uint64 keys, sorted (tile << 32 | depth key)                   */
+    AAA_DBG_VALS = 2,   /* P uint32 Gaussian indices, sorted                                  */
+    AAA_DBG_KEYS_UNSORTED = 3, /* P uint64 keys in emission order                         */
+    AAA_DBG_VALS_UNSORTED = 4, /* P uint32 values in emission order                       */
+    AAA_DBG_RANGES = 5, /* tiles x 2 uint32 [start, end)                                     */
+    AAA_DBG_OVERFLOW = 6 /* overflow tile ids, uint32                                        */
+};
+/* per-Gaussian debug record: v_hat, v_eff, s_hat[3], A, oA, tau, valid(after inside test),
+ * inside, inside_rho2, colour[3], visible (kept by the whole-view cull), crossing,
+ * tile rect tx0, ty0, tx1, ty1 (inclusive; empty if tx0 > tx1), z key (float), pixel rect
+ * x0, x1, y0, y1 (continuous pixel coordinates of the angular bounds) */
+enum { AAA_DBG_GAUSS_FIELDS = 26 };
+
+int32_t aaa_version(void);
+
+/* Create a context on `device`; `cuda_stream` (a cudaStream_t, may be NULL = legacy default
+ * stream) is borrowed, not owned: every kernel and copy of the context is enqueued on it. */
+aaa_status aaa_create(int32_t device, void* cuda_stream, aaa_ctx** out);
+void aaa_destroy(aaa_ctx* ctx);
+aaa_status aaa_set_stream(aaa_ctx* ctx, void* cuda_stream);
+
+aaa_status aaa_default_config(aaa_config* cfg);
+aaa_status aaa_set_config(aaa_ctx* ctx, const aaa_config* cfg);
+
+/* Copy the Gaussians into the context's packed device buffers (caller may free its arrays
+ * when this returns; synchronises). Validates q != 0, s > 0, o in (0,1), finite values,
+ * v_train > 0: on failure returns AAA_ERR_INVALID_GAUSSIAN and writes
+ * the first bad index to *first_bad (nullable). n = 0 is a valid empty scene. */
+aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* first_bad);
+
+/* Validate and store the camera used by aaa_render. */
+aaa_status aaa_set_camera(aaa_ctx* ctx, const aaa_camera* cam);
+
+/* Render the current camera. rgb: 3 x H x W float32 (CHW), T: H x W final transmittance
+ * (nullable). Pointers may be device memory (rendered in place, asynchronous on the
+ * context's stream) or host memory (copied back; the call returns after the copy).
+ * The call synchronises once internally to size the pair buffers. */
+aaa_status aaa_render(aaa_ctx* ctx, float* rgb, float* T);
+
+/* Render n_views cameras (all with the same width/height) into rgb n x 3 x H x W and
+ * T n x H x W (nullable). Same pointer rules as aaa_render. */
+aaa_status aaa_render_batch(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_views, float* rgb, float* T);
+
+/* Render only tile rows [tile_row_begin, tile_row_end) of the current camera (screen-space
+ * band partition for multi-GPU single frames). rgb_band: 3 x band_h x W with
+ * band_h = min(16*tile_row_end, H) - 16*tile_row_begin; T_band nullable. */
+aaa_status aaa_render_tiles(aaa_ctx* ctx, int32_t tile_row_begin, int32_t tile_row_end, float* rgb_band,
+                            float* T_band);
+
+/* Per-tile-row candidate cost of the current camera (sum of candidate tiles of every visible
+ * Gaussian on each tile row), used to balance tile bands; out: ceil(H/16) int64. Syncs. */
+aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows);
+
+aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out); /* synchronises */
+aaa_status aaa_synchronize(aaa_ctx* ctx);
+
+/* Copy an internal buffer of the last render to host memory (parity tests only). *len
+ * receives the byte size; returns AAA_ERR_INVALID_ARG if cap is too small. */
+aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* host_dst, size_t cap, size_t* len);
+
+const char* aaa_last_error(const aaa_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AAA_H_ */

@@ -1,0 +1,124 @@
+// aaa_internal.cuh — device-side layouts and launch entry points shared by the kernels of the
+// B200 forward renderer. See DESIGN.md "Data layout in HBM" for sizes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/aaa.h"
+
+namespace aaa {
+
+constexpr int TILE = 16;                // 16x16 pixel tiles (reading 24)
+constexpr int DEPTH_KEY_BITS = 24;      // depth part of the sort key: f32 bits >> 7 (rounds down)
+constexpr int DEPTH_KEY_SHIFT = 7;
+constexpr int RASTER_REC_F4 = 7;        // raster record: 7 float4 = 112 B
+constexpr float ANGLE_EPS = 1e-4f;      // Eq. 17 epsilon (reading 17)
+constexpr double ZKEY_PAD = 1e-5;       // relative downward pad of the depth key (reading 23)
+
+// Per-view constants passed by value to every kernel (camera in double for the FP64 geometry).
+struct ViewParams {
+    double Rv[9];       // world->view rotation (row-major)
+    double tv[3];       // world->view translation
+    double o[3];        // camera centre in world space, -Rv^T tv
+    double fx, fy, cx, cy, near_z;
+    int width, height;
+    int tiles_x, tiles_y;
+    int tile_row_begin, tile_row_end;   // band [begin, end) of tile rows to emit
+    float k, tau_fixed, alpha_max, T_eps;
+    int tau_mode;
+    float bg[3];
+    uint32_t flags;
+    int sh_degree;
+};
+
+// Scene residency (L0): structure of float4 arrays, 16-byte aligned.
+struct SceneDev {
+    int64_t n;
+    int sh_degree;
+    float4* geomA;   // mu.x, mu.y, mu.z, opacity
+    float4* geomB;   // s.x, s.y, s.z, v_train
+    float4* geomC;   // q.w, q.x, q.y, q.z (normalised at load)
+    float4* sh;      // SoA chunks: sh[c * n + g], c < 3*(deg+1)^2/4 (rounded up); floats in
+                     // coefficient-major, channel-minor order
+    int sh_chunks;
+};
+
+// K3 input per visible Gaussian (80 B): screen-space quadratic q(p) = N(p) - tau Q(p) relative
+// to p_ref (exact tile predicate for non-crossing Gaussians, K3), tile rect, key.
+struct __align__(16) CullRec {
+    double qa, qb, qc, qd, qe, qf;  // q = qa dx^2 + 2 qb dx dy + qc dy^2 + 2 qd dx + 2 qe dy + qf
+    float pref_x, pref_y;
+    uint16_t tx0, ty0, tx1, ty1;    // inclusive tile rect (band-clipped)
+    int32_t cross_slot;             // >= 0: index into CrossRec (exact QP path); -1 otherwise
+    uint32_t zkey;                  // depth key (24 bits)
+};
+
+// Gaussians whose tau-ellipsoid reaches z <= near: the exact QP fallback needs T_view.
+struct CrossRec {
+    double M[9];    // view <- Gaussian-space linear map (row-major), filtered scales
+    double muv[3];
+    double tau;
+    double pad;
+};
+
+// Per-view scratch owned by the context.
+struct ViewBufs {
+    CullRec* cull;        // n
+    float4* raster;       // n * RASTER_REC_F4
+    float4* color;        // n (rgb, unused)
+    uint32_t* counts;     // n candidate tiles per Gaussian
+    uint32_t* offsets;    // n exclusive scan
+    CrossRec* cross;      // n (worst case)
+    double* dbg;          // n * AAA_DBG_GAUSS_FIELDS (only when debugging)
+    // device counters: [0] visible, [1] crossing slots, [2] C total, [3] P pairs,
+    // [4] overflow tiles (K6), [5] overflow quarters (K6b), [6] unresolved pixels (K6c),
+    // [7] tickets (scratch), [8..15] sort tickets, [16] K3 ticket
+    uint32_t* counters;
+    uint32_t* scan_state; // decoupled look-back state for the scan / emit / sort
+};
+
+constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_OVF1 = 4, CNT_OVF2 = 5,
+              CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16,
+              CNT_TOTAL = 32;
+
+// ---- launchers (each file implements its own) ----
+void launch_load_pack(const aaa_gaussians& in, const float* dmeans, const float* dscales, const float* dquats,
+                      const float* dopac, const float* dsh, const float* dvt, SceneDev& sc, int64_t* d_bad,
+                      cudaStream_t st);
+void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bool debug, cudaStream_t st);
+size_t scan_state_words(int64_t n);
+void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, uint32_t* state, uint32_t* ticket,
+                 cudaStream_t st);
+void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, uint64_t* keys,
+                      uint32_t* vals, uint32_t* state, cudaStream_t st);
+struct SortBufs {
+    uint64_t* keys[2];
+    uint32_t* vals[2];
+    uint32_t* hist;        // passes * 256
+    uint32_t* state;       // passes * blocks * 256
+    uint32_t* tickets;     // passes
+    int cap_blocks;
+};
+int sort_passes(int key_bits);
+size_t sort_state_words(uint32_t cap, int passes);
+// returns the index (0/1) of the buffer holding the sorted output
+int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st);
+void launch_ranges(const uint64_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles,
+                   cudaStream_t st);
+struct RasterArgs {
+    const uint64_t* keys;
+    const uint32_t* vals;
+    const uint2* ranges;
+    const float4* raster;
+    const float4* color;
+    float* out_rgb;       // 3 x out_h x W
+    float* out_T;         // out_h x W (nullable)
+    int out_row0;         // first image row stored in out (band renders)
+    int out_h;
+    uint32_t* ovf_list1;  // tiles that overflowed K = window_k
+    uint32_t* ovf_list2;  // (tile, quarter) that overflowed K6b
+    uint32_t* counters;
+};
+void launch_raster(const ViewParams& vp, const RasterArgs& ra, int window_k, cudaStream_t st);
+
+}  // namespace aaa

@@ -1,0 +1,565 @@
+// api.cu — the C ABI (include/aaa.h): context, scene residency, per-view pipeline driver.
+//
+// Pipeline per view (all on the context's stream):
+//   K1 preprocess -> K2 scan -> [one 16-byte D2H of the counters, the only host sync] ->
+//   K3 cull+emit -> K4 onesweep sort -> K5 ranges -> K6 raster (+ K6b / K6c fallbacks).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "aaa_internal.cuh"
+
+using namespace aaa;
+
+struct aaa_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    aaa_config cfg{};
+    aaa_camera cam{};
+    bool have_cam = false, loaded = false;
+    SceneDev scene{};
+    ViewBufs vb{};
+    int64_t vb_n = -1;
+    size_t scan_state_cap = 0;
+    SortBufs sb{};
+    uint32_t pair_cap = 0;
+    size_t sort_state_cap = 0;
+    uint2* ranges = nullptr;
+    int ranges_cap = 0;
+    uint32_t* ovf1 = nullptr;
+    uint32_t* ovf2 = nullptr;
+    int ovf_cap = 0;
+    uint32_t* h_counters = nullptr;  // pinned
+    float* d_out = nullptr;
+    size_t d_out_cap = 0;
+    std::string err;
+    // last view bookkeeping
+    ViewParams last_vp{};
+    uint32_t last_C = 0;
+    int last_sorted = 0;
+    int last_key_bits = 0;
+    float last_ms[8] = {0};
+    cudaEvent_t ev[9] = {};
+    bool events = false;
+};
+
+namespace {
+
+aaa_status fail(aaa_ctx* c, aaa_status s, const std::string& m) {
+    if (c) c->err = m;
+    return s;
+}
+
+#define CU(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? AAA_ERR_OOM : AAA_ERR_CUDA,        \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                      \
+    } while (0)
+
+template <typename T>
+cudaError_t grow(T*& p, size_t& cap, size_t need) {
+    if (need <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    size_t n = need + need / 4 + 256;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    cap = e == cudaSuccess ? n : 0;
+    return e;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+aaa_status check_camera(aaa_ctx* ctx, const aaa_camera* c) {
+    if (!c) return fail(ctx, AAA_ERR_INVALID_ARG, "camera is null");
+    if (c->width < 1 || c->height < 1 || c->width > 65535 || c->height > 65535)
+        return fail(ctx, AAA_ERR_INVALID_ARG, "camera width/height out of range");
+    if (!(c->fx > 0) || !(c->fy > 0) || !(c->near_z > 0) || !std::isfinite(c->cx) || !std::isfinite(c->cy))
+        return fail(ctx, AAA_ERR_INVALID_ARG, "camera fx, fy, near must be > 0 and cx, cy finite");
+    const float* M = c->world_to_view;
+    for (int i = 0; i < 16; i++)
+        if (!std::isfinite(M[i])) return fail(ctx, AAA_ERR_INVALID_ARG, "world_to_view not finite");
+    double R[3][3];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) R[i][j] = M[4 * i + j];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) {
+            double d = R[i][0] * R[j][0] + R[i][1] * R[j][1] + R[i][2] * R[j][2];
+            if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-4)
+                return fail(ctx, AAA_ERR_INVALID_ARG, "world_to_view rotation not orthonormal");
+        }
+    double det = R[0][0] * (R[1][1] * R[2][2] - R[1][2] * R[2][1]) - R[0][1] * (R[1][0] * R[2][2] - R[1][2] * R[2][0]) +
+                 R[0][2] * (R[1][0] * R[2][1] - R[1][1] * R[2][0]);
+    if (det < 0) return fail(ctx, AAA_ERR_INVALID_ARG, "world_to_view rotation has det -1");
+    if (M[12] != 0.f || M[13] != 0.f || M[14] != 0.f || M[15] != 1.f)
+        return fail(ctx, AAA_ERR_INVALID_ARG, "world_to_view last row must be (0,0,0,1)");
+    return AAA_OK;
+}
+
+ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int row_end) {
+    ViewParams vp{};
+    for (int i = 0; i < 3; i++) {
+        for (int j = 0; j < 3; j++) vp.Rv[3 * i + j] = c.world_to_view[4 * i + j];
+        vp.tv[i] = c.world_to_view[4 * i + 3];
+    }
+    // orthonormalise nothing: the camera was validated; o = -Rv^T t
+    for (int i = 0; i < 3; i++) vp.o[i] = -(vp.Rv[i] * vp.tv[0] + vp.Rv[3 + i] * vp.tv[1] + vp.Rv[6 + i] * vp.tv[2]);
+    vp.fx = c.fx; vp.fy = c.fy; vp.cx = c.cx; vp.cy = c.cy; vp.near_z = c.near_z;
+    vp.width = c.width; vp.height = c.height;
+    vp.tiles_x = (c.width + TILE - 1) / TILE;
+    vp.tiles_y = (c.height + TILE - 1) / TILE;
+    vp.tile_row_begin = row_begin;
+    vp.tile_row_end = row_end;
+    vp.k = ctx->cfg.k;
+    vp.tau_fixed = ctx->cfg.tau_fixed;
+    vp.alpha_max = ctx->cfg.alpha_max;
+    vp.T_eps = ctx->cfg.T_eps;
+    vp.tau_mode = ctx->cfg.tau_mode;
+    for (int i = 0; i < 3; i++) vp.bg[i] = ctx->cfg.background[i];
+    vp.flags = ctx->cfg.flags;
+    vp.sh_degree = ctx->scene.sh_degree;
+    return vp;
+}
+
+int bits_for(uint32_t v) {  // bits to represent values < v
+    int b = 0;
+    while ((1ull << b) < v) b++;
+    return b;
+}
+
+aaa_status ensure_view_bufs(aaa_ctx* ctx, int64_t n) {
+    if (ctx->vb_n >= n && ctx->vb.counters) return AAA_OK;
+    ViewBufs& vb = ctx->vb;
+    cudaFree(vb.cull); cudaFree(vb.raster); cudaFree(vb.color); cudaFree(vb.counts); cudaFree(vb.offsets);
+    cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters);
+    uint32_t* keep_state = vb.scan_state;
+    vb = ViewBufs{};
+    vb.scan_state = keep_state;
+    size_t m = (size_t)(n > 0 ? n : 1);
+    CU(cudaMalloc(&vb.cull, m * sizeof(CullRec)));
+    CU(cudaMalloc(&vb.raster, m * RASTER_REC_F4 * sizeof(float4)));
+    CU(cudaMalloc(&vb.color, m * sizeof(float4)));
+    CU(cudaMalloc(&vb.counts, m * sizeof(uint32_t)));
+    CU(cudaMalloc(&vb.offsets, m * sizeof(uint32_t)));
+    CU(cudaMalloc(&vb.cross, m * sizeof(CrossRec)));
+    CU(cudaMalloc(&vb.counters, CNT_TOTAL * sizeof(uint32_t)));
+    ctx->vb_n = n;
+    return AAA_OK;
+}
+
+aaa_status ensure_tiles(aaa_ctx* ctx, int n_tiles) {
+    if (n_tiles <= ctx->ranges_cap) return AAA_OK;
+    cudaFree(ctx->ranges); cudaFree(ctx->ovf1); cudaFree(ctx->ovf2);
+    ctx->ranges = nullptr; ctx->ovf1 = ctx->ovf2 = nullptr;
+    CU(cudaMalloc(&ctx->ranges, (size_t)n_tiles * sizeof(uint2)));
+    CU(cudaMalloc(&ctx->ovf1, (size_t)n_tiles * sizeof(uint32_t)));
+    CU(cudaMalloc(&ctx->ovf2, (size_t)n_tiles * 4 * sizeof(uint32_t)));
+    ctx->ranges_cap = n_tiles;
+    return AAA_OK;
+}
+
+aaa_status ensure_pairs(aaa_ctx* ctx, uint32_t C, int passes) {
+    if (C > ctx->pair_cap || !ctx->sb.keys[0]) {
+        for (int i = 0; i < 2; i++) {
+            cudaFree(ctx->sb.keys[i]);
+            cudaFree(ctx->sb.vals[i]);
+            ctx->sb.keys[i] = nullptr;
+            ctx->sb.vals[i] = nullptr;
+        }
+        uint32_t cap = C + C / 4 + 4096;
+        for (int i = 0; i < 2; i++) {
+            CU(cudaMalloc(&ctx->sb.keys[i], (size_t)cap * sizeof(uint64_t)));
+            CU(cudaMalloc(&ctx->sb.vals[i], (size_t)cap * sizeof(uint32_t)));
+        }
+        ctx->pair_cap = cap;
+        if (!ctx->sb.hist) CU(cudaMalloc(&ctx->sb.hist, 256 * 8 * sizeof(uint32_t)));
+        if (!ctx->sb.tickets) CU(cudaMalloc(&ctx->sb.tickets, 8 * sizeof(uint32_t)));
+    }
+    size_t need = sort_state_words(ctx->pair_cap, 8);
+    CU(grow(ctx->sb.state, ctx->sort_state_cap, need));
+    // K2/K3 look-back state shares one buffer (K2 has finished when this grows)
+    size_t sneed = scan_state_words(ctx->vb_n) + (size_t)ctx->pair_cap / 2048 + 8;
+    CU(grow(ctx->vb.scan_state, ctx->scan_state_cap, sneed));
+    (void)passes;
+    return AAA_OK;
+}
+
+// Run the pipeline for one view into device buffers rgb (3 x out_h x W) / T.
+// stop_after: 1 = after K3 (unsorted pairs kept), 0 = full render.
+aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_end, float* rgb, float* T,
+                    bool debug_k1, int stop_after) {
+    cudaStream_t st = ctx->stream;
+    const int64_t n = ctx->scene.n;
+    ViewParams vp = make_view(ctx, cam, row_begin, row_end);
+    aaa_status s = ensure_view_bufs(ctx, n);
+    if (s) return s;
+    s = ensure_tiles(ctx, vp.tiles_x * vp.tiles_y);
+    if (s) return s;
+    if (debug_k1 && !ctx->vb.dbg) CU(cudaMalloc(&ctx->vb.dbg, (size_t)(n > 0 ? n : 1) * AAA_DBG_GAUSS_FIELDS * sizeof(double)));
+    CU(grow(ctx->vb.scan_state, ctx->scan_state_cap, scan_state_words(n) + 8));
+    const bool timing = (ctx->cfg.flags & AAA_FLAG_TIMING) != 0;
+    if (timing && !ctx->events) {
+        for (int i = 0; i < 9; i++) CU(cudaEventCreate(&ctx->ev[i]));
+        ctx->events = true;
+    }
+    auto mark = [&](int i) {
+        if (timing) cudaEventRecord(ctx->ev[i], st);
+    };
+    CU(cudaMemsetAsync(ctx->vb.counters, 0, CNT_TOTAL * sizeof(uint32_t), st));
+    size_t s2 = scan_state_words(n);
+    CU(cudaMemsetAsync(ctx->vb.scan_state, 0, s2 * sizeof(uint32_t), st));
+    mark(0);
+    launch_preprocess(ctx->scene, vp, ctx->vb, debug_k1, st);
+    mark(1);
+    launch_scan(ctx->vb.counts, ctx->vb.offsets, n, &ctx->vb.counters[CNT_C], ctx->vb.scan_state,
+                &ctx->vb.counters[CNT_SCAN_TICKET], st);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(ctx->h_counters, ctx->vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const uint32_t C = ctx->h_counters[CNT_C];
+    const int key_bits = DEPTH_KEY_BITS + bits_for((uint32_t)(vp.tiles_x * vp.tiles_y));
+    s = ensure_pairs(ctx, C, sort_passes(key_bits));
+    if (s) return s;
+    mark(2);
+    size_t emit_words = (size_t)C / 2048 + 2;
+    CU(cudaMemsetAsync(ctx->vb.scan_state, 0, emit_words * sizeof(uint32_t), st));
+    launch_cull_emit(vp, ctx->vb, n, C, ctx->sb.keys[0], ctx->sb.vals[0], ctx->vb.scan_state, st);
+    mark(3);
+    ctx->last_vp = vp;
+    ctx->last_C = C;
+    ctx->last_key_bits = key_bits;
+    if (stop_after == 1) {
+        ctx->last_sorted = 0;
+        CU(cudaGetLastError());
+        return AAA_OK;
+    }
+    int sorted = launch_sort(ctx->sb, &ctx->vb.counters[CNT_P], C, key_bits, st);
+    ctx->last_sorted = sorted;
+    mark(4);
+    launch_ranges(ctx->sb.keys[sorted], &ctx->vb.counters[CNT_P], C, ctx->ranges, vp.tiles_x * vp.tiles_y, st);
+    mark(5);
+    RasterArgs ra{};
+    ra.keys = ctx->sb.keys[sorted];
+    ra.vals = ctx->sb.vals[sorted];
+    ra.ranges = ctx->ranges;
+    ra.raster = ctx->vb.raster;
+    ra.color = ctx->vb.color;
+    ra.out_rgb = rgb;
+    ra.out_T = T;
+    ra.out_row0 = row_begin * TILE;
+    ra.out_h = std::min(row_end * TILE, cam.height) - row_begin * TILE;
+    ra.ovf_list1 = ctx->ovf1;
+    ra.ovf_list2 = ctx->ovf2;
+    ra.counters = ctx->vb.counters;
+    launch_raster(vp, ra, ctx->cfg.window_k, st);
+    mark(6);
+    CU(cudaGetLastError());
+    return AAA_OK;
+}
+
+aaa_status ensure_out(aaa_ctx* ctx, size_t floats) { CU(grow(ctx->d_out, ctx->d_out_cap, floats)); return AAA_OK; }
+
+aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int row_begin, int row_end, float* rgb,
+                         float* T) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!ctx->loaded) return fail(ctx, AAA_ERR_STATE, "render before aaa_load_gaussians");
+    if (!rgb) return fail(ctx, AAA_ERR_INVALID_ARG, "rgb output is null");
+    const int W = cams[0].width, H = cams[0].height;
+    for (int v = 0; v < n_views; v++) {
+        aaa_status s = check_camera(ctx, &cams[v]);
+        if (s) return s;
+        if (cams[v].width != W || cams[v].height != H)
+            return fail(ctx, AAA_ERR_INVALID_ARG, "all views of a batch need the same width/height");
+    }
+    const int ty = (H + TILE - 1) / TILE;
+    if (row_begin < 0 || row_end > ty || row_begin >= row_end)
+        return fail(ctx, AAA_ERR_INVALID_ARG, "tile row band out of range");
+    const int out_h = std::min(row_end * TILE, H) - row_begin * TILE;
+    const size_t plane = (size_t)out_h * W;
+    const bool dev_rgb = is_device_ptr(rgb);
+    const bool dev_T = T ? is_device_ptr(T) : true;
+    if (!dev_rgb || !dev_T) {
+        aaa_status s = ensure_out(ctx, 4 * plane);
+        if (s) return s;
+    }
+    for (int v = 0; v < n_views; v++) {
+        float* r = dev_rgb ? rgb + 3 * plane * v : ctx->d_out;
+        float* t = T ? (dev_T ? T + plane * v : ctx->d_out + 3 * plane) : nullptr;
+        aaa_status s = run_view(ctx, cams[v], row_begin, row_end, r, t, false, 0);
+        if (s) return s;
+        if (!dev_rgb) CU(cudaMemcpyAsync(rgb + 3 * plane * v, r, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        if (T && !dev_T) CU(cudaMemcpyAsync(T + plane * v, t, plane * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        if (ctx->cfg.flags & AAA_FLAG_TIMING) {
+            CU(cudaEventSynchronize(ctx->ev[6]));
+            for (int i = 0; i < 6; i++) cudaEventElapsedTime(&ctx->last_ms[i], ctx->ev[i], ctx->ev[i + 1]);
+            ctx->last_ms[7] = 0;
+            for (int i = 0; i < 6; i++) ctx->last_ms[7] += ctx->last_ms[i];
+        }
+    }
+    if (!dev_rgb || !dev_T) CU(cudaStreamSynchronize(ctx->stream));
+    return AAA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t aaa_version(void) { return 1; }
+
+aaa_status aaa_create(int32_t device, void* stream, aaa_ctx** out) {
+    if (!out) return AAA_ERR_INVALID_ARG;
+    *out = nullptr;
+    aaa_ctx* ctx = new aaa_ctx();
+    ctx->device = device;
+    ctx->stream = (cudaStream_t)stream;
+    aaa_default_config(&ctx->cfg);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return AAA_ERR_CUDA;
+    }
+    e = cudaMallocHost(&ctx->h_counters, CNT_TOTAL * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        delete ctx;
+        return AAA_ERR_CUDA;
+    }
+    *out = ctx;
+    return AAA_OK;
+}
+
+void aaa_destroy(aaa_ctx* ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    SceneDev& s = ctx->scene;
+    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
+    ViewBufs& vb = ctx->vb;
+    cudaFree(vb.cull); cudaFree(vb.raster); cudaFree(vb.color); cudaFree(vb.counts); cudaFree(vb.offsets);
+    cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
+    for (int i = 0; i < 2; i++) { cudaFree(ctx->sb.keys[i]); cudaFree(ctx->sb.vals[i]); }
+    cudaFree(ctx->sb.hist); cudaFree(ctx->sb.state); cudaFree(ctx->sb.tickets);
+    cudaFree(ctx->ranges); cudaFree(ctx->ovf1); cudaFree(ctx->ovf2); cudaFree(ctx->d_out);
+    if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+    if (ctx->events)
+        for (int i = 0; i < 9; i++) cudaEventDestroy(ctx->ev[i]);
+    delete ctx;
+}
+
+aaa_status aaa_set_stream(aaa_ctx* ctx, void* stream) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    ctx->stream = (cudaStream_t)stream;
+    return AAA_OK;
+}
+
+aaa_status aaa_default_config(aaa_config* c) {
+    if (!c) return AAA_ERR_INVALID_ARG;
+    c->k = 0.3f;
+    c->tau_mode = 0;
+    c->tau_fixed = 9.0f;
+    c->alpha_max = 0.99f;
+    c->T_eps = 1e-4f;
+    c->background[0] = c->background[1] = c->background[2] = 0.f;
+    c->window_k = 16;
+    c->flags = 0;
+    return AAA_OK;
+}
+
+aaa_status aaa_set_config(aaa_ctx* ctx, const aaa_config* c) {
+    if (!ctx || !c) return AAA_ERR_INVALID_ARG;
+    if (!(c->k >= 0) || !(c->alpha_max > 0 && c->alpha_max <= 1) || !(c->T_eps >= 0 && c->T_eps < 1) ||
+        (c->tau_mode != 0 && c->tau_mode != 1) || (c->tau_mode == 1 && !(c->tau_fixed > 0)) ||
+        (c->window_k != 16 && c->window_k != 32))
+        return fail(ctx, AAA_ERR_INVALID_ARG, "invalid config (k>=0, 0<alpha_max<=1, 0<=T_eps<1, tau_mode 0/1, window_k 16/32)");
+    ctx->cfg = *c;
+    return AAA_OK;
+}
+
+aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* first_bad) {
+    if (!ctx || !g) return AAA_ERR_INVALID_ARG;
+    if (first_bad) *first_bad = -1;
+    if (g->n < 0 || g->sh_degree < 0 || g->sh_degree > 3)
+        return fail(ctx, AAA_ERR_INVALID_ARG, "n must be >= 0 and sh_degree in 0..3");
+    if (g->n > 0 && (!g->means || !g->scales || !g->quats || !g->opacities || !g->sh || !g->v_train))
+        return fail(ctx, AAA_ERR_INVALID_ARG, "null scene array");
+    if (g->n >= (1ll << 31)) return fail(ctx, AAA_ERR_INVALID_ARG, "n too large (< 2^31)");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    SceneDev& s = ctx->scene;
+    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
+    s = SceneDev{};
+    ctx->loaded = false;
+    const int64_t n = g->n;
+    const int nf = 3 * (g->sh_degree + 1) * (g->sh_degree + 1);
+    s.n = n;
+    s.sh_degree = g->sh_degree;
+    s.sh_chunks = (nf + 3) / 4;
+    size_t m = (size_t)(n > 0 ? n : 1);
+    CU(cudaMalloc(&s.geomA, m * sizeof(float4)));
+    CU(cudaMalloc(&s.geomB, m * sizeof(float4)));
+    CU(cudaMalloc(&s.geomC, m * sizeof(float4)));
+    CU(cudaMalloc(&s.sh, m * s.sh_chunks * sizeof(float4)));
+    int64_t* d_bad = nullptr;
+    CU(cudaMalloc(&d_bad, sizeof(int64_t)));
+    int64_t init = INT64_MAX;
+    CU(cudaMemcpyAsync(d_bad, &init, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    if (n > 0) {
+        const float *dm = g->means, *ds = g->scales, *dq = g->quats, *dop = g->opacities, *dsh = g->sh, *dv = g->v_train;
+        float* tmp = nullptr;
+        if (!g->device_ptrs) {
+            size_t tot = (size_t)n * (3 + 3 + 4 + 1 + nf + 1);
+            CU(cudaMalloc(&tmp, tot * sizeof(float)));
+            float* p = tmp;
+            auto up = [&](const float* src, size_t cnt, const float*& dst) -> cudaError_t {
+                cudaError_t e = cudaMemcpyAsync(p, src, cnt * sizeof(float), cudaMemcpyHostToDevice, st);
+                dst = p;
+                p += cnt;
+                return e;
+            };
+            CU(up(g->means, (size_t)n * 3, dm));
+            CU(up(g->scales, (size_t)n * 3, ds));
+            CU(up(g->quats, (size_t)n * 4, dq));
+            CU(up(g->opacities, (size_t)n, dop));
+            CU(up(g->sh, (size_t)n * nf, dsh));
+            CU(up(g->v_train, (size_t)n, dv));
+        }
+        launch_load_pack(*g, dm, ds, dq, dop, dsh, dv, s, d_bad, st);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(st));
+        if (tmp) cudaFree(tmp);
+    }
+    int64_t bad = INT64_MAX;
+    CU(cudaMemcpy(&bad, d_bad, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    cudaFree(d_bad);
+    if (bad != INT64_MAX) {
+        if (first_bad) *first_bad = bad;
+        char msg[160];
+        snprintf(msg, sizeof msg,
+                 "Gaussian %lld invalid: need finite values, q != 0, s > 0, 0 < o < 1, v_train > 0 (S:113)",
+                 (long long)bad);
+        return fail(ctx, AAA_ERR_INVALID_GAUSSIAN, msg);
+    }
+    ctx->loaded = true;
+    return AAA_OK;
+}
+
+aaa_status aaa_set_camera(aaa_ctx* ctx, const aaa_camera* cam) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    aaa_status s = check_camera(ctx, cam);
+    if (s) return s;
+    ctx->cam = *cam;
+    ctx->have_cam = true;
+    return AAA_OK;
+}
+
+aaa_status aaa_render(aaa_ctx* ctx, float* rgb, float* T) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "render before aaa_set_camera");
+    const int ty = (ctx->cam.height + TILE - 1) / TILE;
+    return render_common(ctx, &ctx->cam, 1, 0, ty, rgb, T);
+}
+
+aaa_status aaa_render_batch(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_views, float* rgb, float* T) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!cams || n_views < 1) return fail(ctx, AAA_ERR_INVALID_ARG, "need >= 1 camera");
+    const int ty = (cams[0].height + TILE - 1) / TILE;
+    return render_common(ctx, cams, n_views, 0, ty, rgb, T);
+}
+
+aaa_status aaa_render_tiles(aaa_ctx* ctx, int32_t row_begin, int32_t row_end, float* rgb, float* T) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "render before aaa_set_camera");
+    return render_common(ctx, &ctx->cam, 1, row_begin, row_end, rgb, T);
+}
+
+aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
+    if (!ctx || !out) return AAA_ERR_INVALID_ARG;
+    if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
+    const int ty = (ctx->cam.height + TILE - 1) / TILE;
+    if (n_rows < ty) return fail(ctx, AAA_ERR_INVALID_ARG, "n_rows < tile rows");
+    aaa_status s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, false, 1);
+    if (s) return s;
+    uint32_t P = 0;
+    CU(cudaMemcpyAsync(&P, &ctx->vb.counters[CNT_P], sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    std::vector<uint64_t> keys(P);
+    if (P) CU(cudaMemcpy(keys.data(), ctx->sb.keys[0], P * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    const int tx = (ctx->cam.width + TILE - 1) / TILE;
+    for (int r = 0; r < n_rows; r++) out[r] = 0;
+    for (uint32_t i = 0; i < P; i++) out[(keys[i] >> DEPTH_KEY_BITS) / tx]++;
+    return AAA_OK;
+}
+
+aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
+    if (!ctx || !out) return AAA_ERR_INVALID_ARG;
+    CU(cudaStreamSynchronize(ctx->stream));
+    memset(out, 0, sizeof(*out));
+    out->n = ctx->scene.n;
+    if (!ctx->vb.counters) return AAA_OK;
+    uint32_t h[CNT_TOTAL];
+    CU(cudaMemcpy(h, ctx->vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
+    out->visible = h[CNT_VISIBLE];
+    out->candidates = h[CNT_C];
+    out->pairs = h[CNT_P];
+    out->overflow_tiles = h[CNT_OVF1];
+    out->overflow_quarters = h[CNT_OVF2];
+    out->unresolved_pixels = h[CNT_UNRESOLVED];
+    out->crossing = h[CNT_CROSS];
+    for (int i = 0; i < 8; i++) out->ms[i] = ctx->last_ms[i];
+    return AAA_OK;
+}
+
+aaa_status aaa_synchronize(aaa_ctx* ctx) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return AAA_OK;
+}
+
+aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, size_t* len) {
+    if (!ctx || !dst || !len) return AAA_ERR_INVALID_ARG;
+    if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
+    const int ty = (ctx->cam.height + TILE - 1) / TILE;
+    const void* src = nullptr;
+    size_t bytes = 0;
+    aaa_status s = AAA_OK;
+    if (what == AAA_DBG_GAUSS) {
+        s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, true, 1);
+        src = ctx->vb.dbg;
+        bytes = (size_t)ctx->scene.n * AAA_DBG_GAUSS_FIELDS * sizeof(double);
+    } else if (what == AAA_DBG_KEYS_UNSORTED || what == AAA_DBG_VALS_UNSORTED) {
+        s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, false, 1);
+        src = what == AAA_DBG_KEYS_UNSORTED ? (const void*)ctx->sb.keys[0] : (const void*)ctx->sb.vals[0];
+    } else if (what == AAA_DBG_KEYS || what == AAA_DBG_VALS || what == AAA_DBG_RANGES || what == AAA_DBG_OVERFLOW) {
+        src = what == AAA_DBG_KEYS ? (const void*)ctx->sb.keys[ctx->last_sorted]
+            : what == AAA_DBG_VALS ? (const void*)ctx->sb.vals[ctx->last_sorted]
+            : what == AAA_DBG_RANGES ? (const void*)ctx->ranges : (const void*)ctx->ovf1;
+    } else {
+        return fail(ctx, AAA_ERR_INVALID_ARG, "unknown debug buffer");
+    }
+    if (s) return s;
+    CU(cudaStreamSynchronize(ctx->stream));
+    uint32_t h[CNT_TOTAL];
+    CU(cudaMemcpy(h, ctx->vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
+    if (what == AAA_DBG_KEYS || what == AAA_DBG_KEYS_UNSORTED) bytes = (size_t)h[CNT_P] * 8;
+    if (what == AAA_DBG_VALS || what == AAA_DBG_VALS_UNSORTED) bytes = (size_t)h[CNT_P] * 4;
+    if (what == AAA_DBG_RANGES) bytes = (size_t)ctx->last_vp.tiles_x * ctx->last_vp.tiles_y * sizeof(uint2);
+    if (what == AAA_DBG_OVERFLOW) bytes = (size_t)h[CNT_OVF1] * 4;
+    *len = bytes;
+    if (bytes > cap) return fail(ctx, AAA_ERR_INVALID_ARG, "debug buffer too small");
+    if (bytes && src) CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return AAA_OK;
+}
+
+const char* aaa_last_error(const aaa_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

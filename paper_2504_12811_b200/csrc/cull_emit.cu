@@ -1,0 +1,122 @@
+// cull_emit.cu — K3: exact 3D tile-frustum culling (Eq. 18) of every flattened
+// (Gaussian, candidate tile) pair and deterministic emission of (tile, depth) keys.
+//
+// Predicate (keep <=> min over the tile frustum of rho^2 < tau, frustum = the 4 planes through
+// the tile's outermost pixel centres ∩ {z >= near}, readings 20-21):
+//  * tau-ellipsoid entirely beyond near: the minimum over the pixel-centre rectangle of the
+//    exact screen-space quadratic q(p) = |c x w(p)|^2 - tau |w(p)|^2 (q < 0 <=> some ray of the
+//    tile meets the ellipsoid); equivalent to the paper's plane/edge search.
+//  * otherwise (the case where the 2-plane/3-edge shortcut is not exact): the
+//    5-constraint QP by active-set enumeration, in FP64.
+// Emission order is (Gaussian ascending, tile raster order within its rect): a block-wide scan
+// of keep flags plus a decoupled look-back over candidate chunks taken in ticket order.
+#include "aaa_internal.cuh"
+#include "geom.cuh"
+#include "lookback.cuh"
+
+namespace aaa {
+
+constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS;
+
+__global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const CullRec* __restrict__ cull,
+                                                            const CrossRec* __restrict__ cross,
+                                                            const uint32_t* __restrict__ offsets, int64_t n,
+                                                            uint32_t C, uint64_t* __restrict__ keys,
+                                                            uint32_t* __restrict__ vals, uint32_t* counters,
+                                                            uint32_t* state) {
+    __shared__ uint32_t s_scan[32];
+    __shared__ uint32_t s_ticket, s_excl;
+    __shared__ int64_t s_g0;
+    if (threadIdx.x == 0) {
+        uint32_t t = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
+        s_ticket = t;
+        // last Gaussian whose offset <= first candidate of the chunk
+        uint32_t c0 = t * EMIT_CHUNK;
+        int64_t lo = 0, hi = n;  // find largest g with offsets[g] <= c0
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (offsets[mid] <= c0) lo = mid; else hi = mid;
+        }
+        s_g0 = lo;
+    }
+    __syncthreads();
+    uint32_t chunk = s_ticket;
+    uint32_t cbeg = chunk * EMIT_CHUNK + threadIdx.x * EMIT_ITEMS;
+    // this thread's first Gaussian: advance from the chunk's first Gaussian
+    int64_t g = s_g0;
+    {
+        int64_t lo = g, hi = n;
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (offsets[mid] <= cbeg) lo = mid; else hi = mid;
+        }
+        g = lo;
+    }
+    uint64_t key[EMIT_ITEMS];
+    uint32_t val[EMIT_ITEMS];
+    uint32_t keep_mask = 0, nkeep = 0;
+    const bool no_cull = (vp.flags & AAA_FLAG_NO_TILE_CULL) != 0;
+#pragma unroll 1
+    for (int k = 0; k < EMIT_ITEMS; k++) {
+        uint32_t c = cbeg + k;
+        if (c >= C) break;
+        if (g + 1 < n && offsets[g + 1] <= c) {  // next Gaussian with candidates (skip empty runs)
+            int64_t lo = g + 1, hi = n;
+            while (hi - lo > 1) {
+                int64_t mid = (lo + hi) >> 1;
+                if (offsets[mid] <= c) lo = mid; else hi = mid;
+            }
+            g = lo;
+        }
+        const CullRec& r = cull[g];
+        uint32_t j = c - offsets[g];
+        uint32_t w = (uint32_t)r.tx1 - r.tx0 + 1;
+        int tx = r.tx0 + (int)(j % w), ty = r.ty0 + (int)(j / w);
+        double x0 = TILE * tx + 0.5, x1 = fmin(TILE * tx + TILE - 0.5, vp.width - 0.5);
+        double y0 = TILE * ty + 0.5, y1 = fmin(TILE * ty + TILE - 0.5, vp.height - 0.5);
+        bool keep;
+        if (no_cull) {
+            keep = true;
+        } else if (r.cross_slot < 0) {
+            double px = r.pref_x, py = r.pref_y;
+            keep = quad_box_min(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, x0 - px, x1 - px, y0 - py, y1 - py) < 0.0;
+        } else {
+            const CrossRec& cr = cross[r.cross_slot];
+            keep = frustum_qp_min(cr.M, cr.muv, vp.fx, vp.fy, vp.cx, vp.cy, vp.near_z, x0, x1, y0, y1) < cr.tau;
+        }
+        if (keep) {
+            uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
+            key[k] = ((uint64_t)tile << DEPTH_KEY_BITS) | r.zkey;
+            val[k] = (uint32_t)g;
+            keep_mask |= 1u << k;
+            nkeep++;
+        }
+    }
+    uint32_t btot;
+    uint32_t texcl = block_exclusive_scan(nkeep, s_scan, &btot);
+    if (threadIdx.x < 32) {
+        uint32_t e = lookback_warp(state, chunk, btot);
+        if (threadIdx.x == 0) s_excl = e;
+    }
+    __syncthreads();
+    uint32_t pos = s_excl + texcl;
+#pragma unroll
+    for (int k = 0; k < EMIT_ITEMS; k++) {
+        if (keep_mask & (1u << k)) {
+            keys[pos] = key[k];
+            vals[pos] = val[k];
+            pos++;
+        }
+    }
+    if (threadIdx.x == 0 && (uint64_t)(chunk + 1) * EMIT_CHUNK >= C) counters[CNT_P] = s_excl + btot;
+}
+
+void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, uint64_t* keys,
+                      uint32_t* vals, uint32_t* state, cudaStream_t st) {
+    if (C == 0) return;
+    unsigned blocks = (C + EMIT_CHUNK - 1) / EMIT_CHUNK;
+    k_cull_emit<<<blocks, EMIT_THREADS, 0, st>>>(vp, vb.cull, vb.cross, vb.offsets, n, C, keys, vals, vb.counters,
+                                                 state);
+}
+
+}  // namespace aaa

@@ -1,0 +1,373 @@
+// preprocess.cu — L0 scene packing and K1, the per-Gaussian preprocess kernel.
+//
+// K1 (one thread per Gaussian; HBM-bound: 48 B geometry + SH of survivors in, ~200 B out):
+//   filter      v_hat = f/z (Eq. 6), v' = min(v_train, v_hat) (Eq. 13),
+//               s_hat_i = s_i^2 + k/v'^2 and the perpendicular amplitude A (Eq. 12);
+//   tau         2 ln(255 o A) (DESIGN reading 1); camera-inside discard;
+//   bounds      view-space tangent-plane angles (Eq. 14-15) with the rotation step
+//               (Eq. 16) and clamp (Eq. 17), full axis on a negative
+//               discriminant; readings 16-19;
+//   view cull   exact min of rho^2 over the view frustum — screen-space quadratic box
+//               minimum when the ellipsoid lies beyond near, 5-plane QP otherwise;
+//   key         tight lower bound of the per-ray max-response depth (reading 23);
+//   records     K3 cull record (FP64 quadratic), K6 raster record (FP32, re-centred at p_ref).
+// Geometry runs in FP64 (B200 has full-rate-class FP64 for this per-Gaussian work).
+#include <math_constants.h>
+
+#include "aaa_internal.cuh"
+#include "geom.cuh"
+
+namespace aaa {
+
+// ------------------------------------------------------------------ L0: validate + pack
+__global__ void k_load_pack(int64_t n, int deg, const float* __restrict__ means, const float* __restrict__ scales,
+                            const float* __restrict__ quats, const float* __restrict__ opac,
+                            const float* __restrict__ sh, const float* __restrict__ vt, float4* geomA,
+                            float4* geomB, float4* geomC, float4* shp, int chunks,
+                            unsigned long long* first_bad) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    float mx = means[3 * g], my = means[3 * g + 1], mz = means[3 * g + 2];
+    float sx = scales[3 * g], sy = scales[3 * g + 1], sz = scales[3 * g + 2];
+    float qw = quats[4 * g], qx = quats[4 * g + 1], qy = quats[4 * g + 2], qz = quats[4 * g + 3];
+    float o = opac[g], v = vt[g];
+    bool ok = isfinite(mx) && isfinite(my) && isfinite(mz) && isfinite(sx) && isfinite(sy) && isfinite(sz) &&
+              sx > 0.f && sy > 0.f && sz > 0.f && isfinite(qw) && isfinite(qx) && isfinite(qy) && isfinite(qz) &&
+              o > 0.f && o < 1.f && v > 0.f && !isnan(v);
+    double qn = sqrt((double)qw * qw + (double)qx * qx + (double)qy * qy + (double)qz * qz);
+    ok = ok && qn > 0.0;
+    int nf = 3 * (deg + 1) * (deg + 1);
+    const float* s = sh + g * nf;
+    for (int i = 0; i < nf; i++) ok = ok && isfinite(s[i]);
+    if (!ok) atomicMin(first_bad, (unsigned long long)g);
+    geomA[g] = make_float4(mx, my, mz, o);
+    geomB[g] = make_float4(sx, sy, sz, v);
+    geomC[g] = ok ? make_float4((float)(qw / qn), (float)(qx / qn), (float)(qy / qn), (float)(qz / qn))
+                  : make_float4(1.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < chunks; c++) {
+        float e[4];
+        for (int j = 0; j < 4; j++) e[j] = (4 * c + j < nf) ? s[4 * c + j] : 0.f;
+        shp[(int64_t)c * n + g] = make_float4(e[0], e[1], e[2], e[3]);
+    }
+}
+
+void launch_load_pack(const aaa_gaussians& in, const float* dm, const float* ds, const float* dq, const float* dop,
+                      const float* dsh, const float* dvt, SceneDev& sc, int64_t* d_bad, cudaStream_t st) {
+    if (sc.n == 0) return;
+    int threads = 256;
+    unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
+    k_load_pack<<<blocks, threads, 0, st>>>(sc.n, sc.sh_degree, dm, ds, dq, dop, dsh, dvt, sc.geomA, sc.geomB,
+                                            sc.geomC, sc.sh, sc.sh_chunks, (unsigned long long*)d_bad);
+}
+
+// ------------------------------------------------------------------ K1 helpers
+// Spherical-harmonic colour, degree <= 3, 3DGS real basis (reading 15), direction d (unit).
+__device__ __forceinline__ void sh_color(const float4* __restrict__ sh, int64_t n, int64_t g, int deg, float3 d,
+                                         float out[3]) {
+    float f[48];
+    int chunks = (3 * (deg + 1) * (deg + 1) + 3) / 4;
+#pragma unroll
+    for (int c = 0; c < 12; c++) {
+        if (c < chunks) {
+            float4 v = __ldg(&sh[(int64_t)c * n + g]);
+            f[4 * c] = v.x; f[4 * c + 1] = v.y; f[4 * c + 2] = v.z; f[4 * c + 3] = v.w;
+        } else {
+            f[4 * c] = f[4 * c + 1] = f[4 * c + 2] = f[4 * c + 3] = 0.f;
+        }
+    }
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    const float C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f, -1.0925484305920792f,
+                         0.5462742152960396f};
+    const float C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f, 0.3731763325901154f,
+                         -0.4570457994644658f, 1.445305721320277f, -0.5900435899266435f};
+    float x = d.x, y = d.y, z = d.z;
+    float b[16];
+    b[0] = C0;
+    b[1] = -C1 * y; b[2] = C1 * z; b[3] = -C1 * x;
+    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    b[4] = C2[0] * xy; b[5] = C2[1] * yz; b[6] = C2[2] * (2.f * zz - xx - yy); b[7] = C2[3] * xz;
+    b[8] = C2[4] * (xx - yy);
+    b[9] = C3[0] * y * (3.f * xx - yy); b[10] = C3[1] * xy * z; b[11] = C3[2] * y * (4.f * zz - xx - yy);
+    b[12] = C3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy); b[13] = C3[4] * x * (4.f * zz - xx - yy);
+    b[14] = C3[5] * z * (xx - yy); b[15] = C3[6] * x * (xx - 3.f * yy);
+    int K = (deg + 1) * (deg + 1);
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            if (k < K) acc = fmaf(b[k], f[3 * k + ch], acc);
+        out[ch] = fmaxf(acc + 0.5f, 0.f);
+    }
+}
+
+// One screen axis of the view-space bounds (Eq. 14-17). s_ii, s_i3, s33: the quadric
+// coefficients of Appendix B; disc: cancellation-free discriminant s_i3^2 - s_ii s33.
+// Returns false when no front-facing ray of this plane family meets the ellipsoid.
+__device__ bool axis_bounds(double s_ii, double s_i3, double s33, double disc, double mu_i, double mu_z, double f,
+                            double c, double& lo, double& hi) {
+    const double PI = CUDART_PI;
+    if (!(disc >= 0.0)) {  // the ellipsoid meets the plane family's axis: full axis
+        lo = -CUDART_INF;
+        hi = CUDART_INF;
+        return true;
+    }
+    double sq = sqrt(disc);
+    double num = s_i3 + copysign(sq, s_i3);
+    if (num == 0.0) {
+        lo = -CUDART_INF;
+        hi = CUDART_INF;
+        return true;
+    }
+    double r1 = atan2(num, s33);   // tan r1 = (s_i3 +- sqrt(D)) / s33
+    double r2 = atan2(s_ii, num);  // tan r2 = s_ii / (s_i3 +- sqrt(D)) (the other root, stable form)
+    // rotation step (Eq. 16): representatives in (theta_mu - pi, theta_mu] (reading 16)
+    double tm = atan2(mu_i, mu_z);
+    r1 += PI * floor((tm - r1) / PI);
+    r2 += PI * floor((tm - r2) / PI);
+    double t1 = fmax(r1, r2);
+    double t2 = fmin(r1, r2) + PI;
+    // the ray-angle interval [t1, t2] (length < pi) -> its copy meeting the front half (-pi/2, pi/2)
+    bool found = false;
+    for (int m = -1; m <= 1; m++) {
+        double a = t1 + 2.0 * PI * m, b = t2 + 2.0 * PI * m;
+        if (b > -0.5 * PI && a < 0.5 * PI) {
+            t1 = a;
+            t2 = b;
+            found = true;
+            break;
+        }
+    }
+    if (!found) return false;
+    // clamp (Eq. 17)
+    t1 = fmax(t1, -0.5 * PI + (double)ANGLE_EPS);
+    t2 = fmin(t2, 0.5 * PI - (double)ANGLE_EPS);
+    lo = f * tan(t1) + c;
+    hi = f * tan(t2) + c;
+    return true;
+}
+
+// ------------------------------------------------------------------ K1
+__global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, ViewParams vp, ViewBufs vb, int debug) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= sc.n) return;
+    const double INF = CUDART_INF;
+    float4 A4 = __ldg(&sc.geomA[g]), B4 = __ldg(&sc.geomB[g]), C4 = __ldg(&sc.geomC[g]);
+    double* dbg = debug ? vb.dbg + g * AAA_DBG_GAUSS_FIELDS : nullptr;
+    if (dbg)
+        for (int i = 0; i < AAA_DBG_GAUSS_FIELDS; i++) dbg[i] = 0.0;
+    vb.counts[g] = 0;
+
+    double mu[3] = {A4.x, A4.y, A4.z};
+    double s[3] = {B4.x, B4.y, B4.z};
+    double R[9];
+    quat_to_rot(C4, R);
+    double muv[3];
+    mat3_vec(vp.Rv, mu, muv);
+    for (int i = 0; i < 3; i++) muv[i] += vp.tv[i];
+
+    // --- adaptive 3D filter (Eq. 6, 12, 13)
+    double f = fmax(vp.fx, vp.fy);
+    double vhat = muv[2] > 0.0 ? f / muv[2] : INF;
+    double veff = fmin((double)B4.w, vhat);
+    double cf = isinf(veff) ? 0.0 : (double)vp.k / (veff * veff);
+    double shat[3], sig[3];
+    for (int i = 0; i < 3; i++) {
+        shat[i] = s[i] * s[i] + cf;
+        sig[i] = sqrt(shat[i]);
+    }
+    double d[3] = {mu[0] - vp.o[0], mu[1] - vp.o[1], mu[2] - vp.o[2]};
+    double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    for (int i = 0; i < 3; i++) d[i] /= dn;
+    double Amp = 1.0;
+    if (cf > 0.0) {  // Eq. 12 with d' = R^T d (Eq. 11)
+        double dp0 = R[0] * d[0] + R[3] * d[1] + R[6] * d[2];
+        double dp1 = R[1] * d[0] + R[4] * d[1] + R[7] * d[2];
+        double dp2 = R[2] * d[0] + R[5] * d[1] + R[8] * d[2];
+        double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+        double num = dp0 * dp0 * s2[1] * s2[2] + dp1 * dp1 * s2[0] * s2[2] + dp2 * dp2 * s2[0] * s2[1];
+        double den = dp0 * dp0 * shat[1] * shat[2] + dp1 * dp1 * shat[0] * shat[2] + dp2 * dp2 * shat[0] * shat[1];
+        Amp = sqrt(num / den);
+    }
+    double oA = (double)A4.w * Amp;
+    double tau = 2.0 * log(255.0 * oA);
+    if (vp.tau_mode == 1) tau = fmin((double)vp.tau_fixed, tau);
+    if (dbg) {
+        dbg[0] = vhat; dbg[1] = veff; dbg[2] = shat[0]; dbg[3] = shat[1]; dbg[4] = shat[2];
+        dbg[5] = Amp; dbg[6] = oA; dbg[7] = tau;
+    }
+    if (!(tau > 0.0)) return;
+
+    // --- T_view linear part M = Rv R diag(sig); W = M^-1 = diag(1/sig) (Rv R)^T; c = -W mu_v
+    double Q[9];
+    mat3_mul(vp.Rv, R, Q);
+    double M[9];
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) M[3 * i + j] = Q[3 * i + j] * sig[j];
+    double Wm[9];
+    for (int j = 0; j < 3; j++)
+        for (int i = 0; i < 3; i++) Wm[3 * j + i] = Q[3 * i + j] / sig[j];
+    double c[3];
+    mat3_vec(Wm, muv, c);
+    for (int i = 0; i < 3; i++) c[i] = -c[i];
+    double c2 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+    bool inside = c2 < tau;  // camera inside the tau-ellipsoid
+    if (dbg) {
+        dbg[8] = inside ? 0.0 : 1.0;
+        dbg[9] = inside ? 1.0 : 0.0;
+        dbg[10] = c2;
+    }
+    if (inside) return;
+
+    // --- depth extent; entirely closer than near -> no pixel can take it (reading 6)
+    double gz[3] = {M[6], M[7], M[8]};
+    double szz = gz[0] * gz[0] + gz[1] * gz[1] + gz[2] * gz[2];
+    double zext = sqrt(tau * szz);
+    if (muv[2] + zext < vp.near_z) return;
+    bool crossing = (muv[2] - zext) <= vp.near_z;
+
+    // --- bounds (Eq. 14-17): s_ij = tau (M M^T)_ij - mu_i mu_j, discriminant cancellation-free
+    const double* Mx = &M[0];
+    const double* My = &M[3];
+    const double* Mz = &M[6];
+    double sxx = tau * dot3(Mx, Mx) - muv[0] * muv[0];
+    double sxz = tau * dot3(Mx, Mz) - muv[0] * muv[2];
+    double syy = tau * dot3(My, My) - muv[1] * muv[1];
+    double syz = tau * dot3(My, Mz) - muv[1] * muv[2];
+    double szz3 = tau * szz - muv[2] * muv[2];
+    double ex[3], ey[3], cxz[3], cyz[3];
+    for (int j = 0; j < 3; j++) {
+        ex[j] = muv[2] * Mx[j] - muv[0] * Mz[j];
+        ey[j] = muv[2] * My[j] - muv[1] * Mz[j];
+    }
+    cross3(Mx, Mz, cxz);
+    cross3(My, Mz, cyz);
+    double discx = tau * (dot3(ex, ex) - tau * dot3(cxz, cxz));
+    double discy = tau * (dot3(ey, ey) - tau * dot3(cyz, cyz));
+    double xlo, xhi, ylo, yhi;
+    if (!axis_bounds(sxx, sxz, szz3, discx, muv[0], muv[2], vp.fx, vp.cx, xlo, xhi)) return;
+    if (!axis_bounds(syy, syz, szz3, discy, muv[1], muv[2], vp.fy, vp.cy, ylo, yhi)) return;
+    if (dbg) {
+        dbg[21] = xlo; dbg[22] = xhi; dbg[23] = ylo; dbg[24] = yhi;
+    }
+    // pixel-centre index range with 1 px padding, clipped to the image
+    const double PAD = 1.0;
+    double ixlo = ceil(fmax(xlo - PAD - 0.5, -1.0)), ixhi = floor(fmin(xhi + PAD - 0.5, (double)vp.width));
+    double iylo = ceil(fmax(ylo - PAD - 0.5, -1.0)), iyhi = floor(fmin(yhi + PAD - 0.5, (double)vp.height));
+    int i0 = max(0, (int)ixlo), i1 = min(vp.width - 1, (int)ixhi);
+    int j0 = max(0, (int)iylo), j1 = min(vp.height - 1, (int)iyhi);
+    if (i0 > i1 || j0 > j1) return;
+
+    // --- p_ref: projected mean clamped into the pixel rect, else the rect centre (rounded to f32)
+    double px0 = i0 + 0.5, px1 = i1 + 0.5, py0 = j0 + 0.5, py1 = j1 + 0.5;
+    double prx, pry;
+    if (muv[2] > 0.0) {
+        prx = fmin(fmax(vp.fx * muv[0] / muv[2] + vp.cx, px0), px1);
+        pry = fmin(fmax(vp.fy * muv[1] / muv[2] + vp.cy, py0), py1);
+    } else {
+        prx = 0.5 * (px0 + px1);
+        pry = 0.5 * (py0 + py1);
+    }
+    float prx_f = (float)prx, pry_f = (float)pry;
+    prx = prx_f;
+    pry = pry_f;
+    // pixel ray r(p) = ((px-cx)/fx, (py-cy)/fy, 1); unit-space direction w(p) = W r(p) is affine in p
+    double rref[3] = {(prx - vp.cx) / vp.fx, (pry - vp.cy) / vp.fy, 1.0};
+    double wref[3], wa[3], wb[3];
+    mat3_vec(Wm, rref, wref);
+    for (int j = 0; j < 3; j++) {
+        wa[j] = Wm[3 * j + 0] / vp.fx;
+        wb[j] = Wm[3 * j + 1] / vp.fy;
+    }
+    // rho^2(p) = |c x w(p)|^2 / |w(p)|^2,  c x w(p) = F0 + dx E1 + dy E2 (re-centred, DESIGN K6)
+    double F0[3], E1[3], E2[3];
+    cross3(c, wref, F0);
+    cross3(c, wa, E1);
+    cross3(c, wb, E2);
+    // screen-space quadratic q(p) = |c x w|^2 - tau |w|^2 (< 0 <=> rho^2 < tau), relative to p_ref
+    double qa = dot3(E1, E1) - tau * dot3(wa, wa);
+    double qb = dot3(E1, E2) - tau * dot3(wa, wb);
+    double qc = dot3(E2, E2) - tau * dot3(wb, wb);
+    double qd = dot3(F0, E1) - tau * dot3(wref, wa);
+    double qe = dot3(F0, E2) - tau * dot3(wref, wb);
+    double qf = dot3(F0, F0) - tau * dot3(wref, wref);
+
+    // --- whole-view frustum cull, exact: over the bounds rect (which holds every pixel
+    // centre of the tau-ellipsoid's projection), quadratic box minimum or the 5-plane QP
+    bool visible;
+    if (!crossing) {
+        visible = quad_box_min(qa, qb, qc, qd, qe, qf, px0 - prx, px1 - prx, py0 - pry, py1 - pry) < 0.0;
+    } else {
+        visible = frustum_qp_min(M, muv, vp.fx, vp.fy, vp.cx, vp.cy, vp.near_z, px0, px1, py0, py1) < tau;
+    }
+    if (dbg) dbg[15] = crossing ? 1.0 : 0.0;
+    if (!visible) return;
+
+    // --- tile rect, band-clipped
+    int tx0 = i0 / TILE, tx1 = i1 / TILE, ty0 = j0 / TILE, ty1 = j1 / TILE;
+    ty0 = max(ty0, vp.tile_row_begin);
+    ty1 = min(ty1, vp.tile_row_end - 1);
+
+    // --- depth key: tight lower bound of z* over every contributing ray (reading 23)
+    double cn = sqrt(c2);
+    double ch[3] = {c[0] / cn, c[1] / cn, c[2] / cn};
+    double gc = dot3(gz, ch);
+    double gp[3] = {gz[0] - gc * ch[0], gz[1] - gc * ch[1], gz[2] - gc * ch[2]};
+    double zlb = muv[2] - sqrt(tau) * sqrt(dot3(gp, gp)) - (tau / cn) * fmax(0.0, -gc);
+    zlb = fmax(zlb, vp.near_z);
+    float zf = __double2float_rd(zlb * (1.0 - ZKEY_PAD));
+    uint32_t zkey = __float_as_uint(zf) >> DEPTH_KEY_SHIFT;
+
+    // --- colour (reading 15): SH at d = (mu - o)/|mu - o|
+    float rgb[3];
+    sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
+
+    int slot = -1;
+    if (crossing) {
+        slot = (int)atomicAdd(&vb.counters[CNT_CROSS], 1u);
+        CrossRec cr;
+        for (int i = 0; i < 9; i++) cr.M[i] = M[i];
+        for (int i = 0; i < 3; i++) cr.muv[i] = muv[i];
+        cr.tau = tau;
+        cr.pad = 0.0;
+        vb.cross[slot] = cr;
+    }
+    CullRec cu;
+    cu.qa = qa; cu.qb = qb; cu.qc = qc; cu.qd = qd; cu.qe = qe; cu.qf = qf;
+    cu.pref_x = prx_f;
+    cu.pref_y = pry_f;
+    cu.tx0 = (uint16_t)tx0; cu.ty0 = (uint16_t)ty0; cu.tx1 = (uint16_t)tx1; cu.ty1 = (uint16_t)ty1;
+    cu.cross_slot = slot;
+    cu.zkey = zkey;
+    vb.cull[g] = cu;
+
+    float4* rr = vb.raster + g * RASTER_REC_F4;
+    rr[0] = make_float4(prx_f, pry_f, (float)oA, (float)tau);
+    rr[1] = make_float4((float)F0[0], (float)F0[1], (float)F0[2], (float)E1[0]);
+    rr[2] = make_float4((float)E1[1], (float)E1[2], (float)E2[0], (float)E2[1]);
+    rr[3] = make_float4((float)E2[2], (float)wref[0], (float)wref[1], (float)wref[2]);
+    rr[4] = make_float4((float)wa[0], (float)wa[1], (float)wa[2], (float)wb[0]);
+    rr[5] = make_float4((float)wb[1], (float)wb[2], (float)dot3(c, wref), (float)dot3(c, wa));
+    rr[6] = make_float4((float)dot3(c, wb), 0.f, 0.f, 0.f);
+    vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+
+    uint32_t cnt = (ty0 <= ty1) ? (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1) : 0u;
+    vb.counts[g] = cnt;
+    atomicAdd(&vb.counters[CNT_VISIBLE], 1u);
+    if (dbg) {
+        dbg[11] = rgb[0]; dbg[12] = rgb[1]; dbg[13] = rgb[2];
+        dbg[14] = 1.0;
+        dbg[16] = tx0; dbg[17] = ty0; dbg[18] = tx1; dbg[19] = ty1;
+        dbg[20] = (double)__uint_as_float(zkey << DEPTH_KEY_SHIFT);
+        dbg[25] = zlb;
+    }
+}
+
+void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bool debug, cudaStream_t st) {
+    if (sc.n == 0) return;
+    int threads = 128;
+    unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
+    k_preprocess<<<blocks, threads, 0, st>>>(sc, vp, vb, debug ? 1 : 0);
+}
+
+}  // namespace aaa

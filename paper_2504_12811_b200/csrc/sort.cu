@@ -1,0 +1,208 @@
+// sort.cu — K4: stable LSD onesweep radix sort of the (tile, depth) keys with their Gaussian
+// indices, and K5: per-tile [start, end) ranges of the sorted list.
+//
+// The paper does not name its sort; the global (tile, depth) order is the
+// first level of the hierarchical re-sort. Design (B200, HBM-bound):
+//  * one upfront histogram pass computes the 256-bin digit histograms of every pass at once
+//    (reads 8 B per key once);
+//  * each digit pass is one kernel: a CTA ranks 4096 keys with warp-level multisplit
+//    (match.any + popc, stable within the warp), publishes its per-digit counts with a
+//    decoupled look-back over CTAs taken in ticket order, reorders the keys in shared memory
+//    and writes digit runs (reads 12 B, writes 12 B per key per pass).
+// Key layout: tile << 24 | depth24 (depth24 = f32 bits >> 7 of a positive lower bound, so
+// truncation rounds down and keeps the bound valid). Key bits = 24 + tile bits; 8-bit digits.
+#include "aaa_internal.cuh"
+#include "lookback.cuh"
+
+namespace aaa {
+
+constexpr int SORT_THREADS = 256, SORT_ITEMS = 16, SORT_TILE = SORT_THREADS * SORT_ITEMS, SORT_WARPS = 8;
+constexpr int MAX_PASSES = 8;
+
+int sort_passes(int key_bits) { return (key_bits + 7) / 8; }
+
+size_t sort_state_words(uint32_t cap, int passes) {
+    size_t blocks = (cap + SORT_TILE - 1) / SORT_TILE + 1;
+    return (size_t)passes * blocks * 256;
+}
+
+__global__ void __launch_bounds__(256) k_sort_hist(const uint64_t* __restrict__ keys, const uint32_t* d_count,
+                                                    int passes, uint32_t* hist) {
+    __shared__ uint32_t sh[MAX_PASSES * 256];
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    uint32_t P = *d_count;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        for (int p = 0; p < passes; p++) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 0xFF)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// exclusive scan of each pass's 256-bin histogram, in place (one CTA of 256 threads per pass)
+__global__ void k_sort_hist_scan(uint32_t* hist) {
+    __shared__ uint32_t s_scan[32];
+    uint32_t* h = hist + blockIdx.x * 256;
+    uint32_t v = h[threadIdx.x], tot;
+    uint32_t e = block_exclusive_scan(v, s_scan, &tot);
+    h[threadIdx.x] = e;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __restrict__ kin,
+                                                           const uint32_t* __restrict__ vin,
+                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                           const uint32_t* d_count, int shift,
+                                                           const uint32_t* __restrict__ digit_base,
+                                                           uint32_t* state, uint32_t* ticket_ctr) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);                       // SORT_TILE
+    uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + SORT_TILE);          // SORT_TILE
+    uint32_t* s_whist = s_vals + SORT_TILE;                                      // SORT_WARPS * 256
+    uint32_t* s_base = s_whist + SORT_WARPS * 256;                               // 256 (global base per digit)
+    uint32_t* s_bin = s_base + 256;                                              // 256 (block-local start)
+    uint32_t* s_scan = s_bin + 256;                                              // 32
+    uint32_t* s_ticket = s_scan + 32;
+
+    const uint32_t P = *d_count;
+    if (threadIdx.x == 0) *s_ticket = atomicAdd(ticket_ctr, 1u);
+    for (int i = threadIdx.x; i < SORT_WARPS * 256; i += SORT_THREADS) s_whist[i] = 0;
+    __syncthreads();
+    const uint32_t b = *s_ticket;
+    const uint64_t start = (uint64_t)b * SORT_TILE;
+    if (start >= P) return;  // no later ticket looks back past the last real block
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+
+    uint64_t k[SORT_ITEMS];
+    uint32_t v[SORT_ITEMS];
+    uint32_t rank[SORT_ITEMS];
+    // warp w owns the contiguous segment [w*512, w*512+512) of the tile, round r covers 32 keys
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; r++) {
+        uint64_t idx = start + w * (SORT_ITEMS * 32) + r * 32 + lane;
+        bool valid = idx < P;
+        k[r] = valid ? kin[idx] : ~0ull;
+        v[r] = valid ? vin[idx] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; r++) {
+        uint64_t idx = start + w * (SORT_ITEMS * 32) + r * 32 + lane;
+        bool valid = idx < P;
+        uint32_t d = valid ? (uint32_t)((k[r] >> shift) & 0xFF) : (0x100u | lane);
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t prev = valid ? s_whist[w * 256 + d] : 0u;
+        __syncwarp();
+        if (valid && (peers & lt_mask) == 0) s_whist[w * 256 + d] = prev + __popc(peers);
+        __syncwarp();
+        rank[r] = prev + __popc(peers & lt_mask);
+    }
+    __syncthreads();
+    // per digit (thread = digit): across-warp exclusive prefix, block total, look-back
+    {
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < SORT_WARPS; ww++) {
+            uint32_t c = s_whist[ww * 256 + d];
+            s_whist[ww * 256 + d] = run;
+            run += c;
+        }
+        uint32_t tot;
+        uint32_t bin = block_exclusive_scan(run, s_scan, &tot);
+        s_bin[d] = bin;
+        // decoupled look-back for digit d over earlier tickets
+        uint32_t* st = state + (size_t)b * 256 + d;
+        uint32_t excl = 0;
+        if (b == 0) {
+            lb_store(st, LB_PRE | run);
+        } else {
+            lb_store(st, LB_AGG | run);
+            int64_t j = (int64_t)b - 1;
+            while (j >= 0) {
+                uint32_t sv;
+                do {
+                    sv = lb_load(state + (size_t)j * 256 + d);
+                } while ((sv & ~LB_VAL) == 0);
+                excl += sv & LB_VAL;
+                if ((sv & ~LB_VAL) == LB_PRE) break;
+                j--;
+            }
+            lb_store(st, LB_PRE | (excl + run));
+        }
+        s_base[d] = digit_base[d] + excl - bin;
+    }
+    __syncthreads();
+    // reorder in shared memory (block-stable order), then write digit runs
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; r++) {
+        uint64_t idx = start + w * (SORT_ITEMS * 32) + r * 32 + lane;
+        if (idx < P) {
+            uint32_t d = (uint32_t)((k[r] >> shift) & 0xFF);
+            uint32_t pos = s_bin[d] + s_whist[w * 256 + d] + rank[r];
+            s_keys[pos] = k[r];
+            s_vals[pos] = v[r];
+        }
+    }
+    __syncthreads();
+    uint32_t nvalid = (uint32_t)min((uint64_t)SORT_TILE, (uint64_t)P - start);
+    for (uint32_t i = threadIdx.x; i < nvalid; i += SORT_THREADS) {
+        uint64_t key = s_keys[i];
+        uint32_t d = (uint32_t)((key >> shift) & 0xFF);
+        uint32_t o = s_base[d] + i;
+        kout[o] = key;
+        vout[o] = s_vals[i];
+    }
+}
+
+static size_t onesweep_smem() {
+    return (size_t)SORT_TILE * 12 + (SORT_WARPS * 256 + 256 + 256 + 32 + 4) * 4;
+}
+
+int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st) {
+    int passes = sort_passes(key_bits);
+    if (cap == 0) return 0;
+    unsigned blocks = (cap + SORT_TILE - 1) / SORT_TILE;
+    size_t per_pass = (size_t)(blocks + 1) * 256;
+    cudaMemsetAsync(sb.hist, 0, sizeof(uint32_t) * 256 * passes, st);
+    cudaMemsetAsync(sb.state, 0, sizeof(uint32_t) * per_pass * passes, st);
+    cudaMemsetAsync(sb.tickets, 0, sizeof(uint32_t) * passes, st);
+    unsigned hblocks = min(blocks, 148u * 4u);
+    k_sort_hist<<<hblocks, 256, 0, st>>>(sb.keys[0], d_count, passes, sb.hist);
+    k_sort_hist_scan<<<passes, 256, 0, st>>>(sb.hist);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem());
+        attr = true;
+    }
+    int cur = 0;
+    for (int p = 0; p < passes; p++) {
+        k_onesweep<<<blocks, SORT_THREADS, onesweep_smem(), st>>>(sb.keys[cur], sb.vals[cur], sb.keys[cur ^ 1],
+                                                                   sb.vals[cur ^ 1], d_count, 8 * p,
+                                                                   sb.hist + 256 * p, sb.state + per_pass * p,
+                                                                   sb.tickets + p);
+        cur ^= 1;
+    }
+    return cur;
+}
+
+// ------------------------------------------------------------------ K5: tile ranges
+__global__ void k_ranges(const uint64_t* __restrict__ keys, const uint32_t* d_count, uint2* ranges) {
+    uint32_t P = *d_count;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        uint32_t t = (uint32_t)(keys[i] >> DEPTH_KEY_BITS);
+        if (i == 0 || (uint32_t)(keys[i - 1] >> DEPTH_KEY_BITS) != t) ranges[t].x = i;
+        if (i + 1 == P || (uint32_t)(keys[i + 1] >> DEPTH_KEY_BITS) != t) ranges[t].y = i + 1;
+    }
+}
+
+void launch_ranges(const uint64_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles,
+                   cudaStream_t st) {
+    cudaMemsetAsync(ranges, 0, sizeof(uint2) * n_tiles, st);
+    if (cap == 0) return;
+    unsigned blocks = min((cap + 255) / 256, 148u * 8u);
+    k_ranges<<<blocks, 256, 0, st>>>(keys, d_count, ranges);
+}
+
+}  // namespace aaa

@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the float64 oracle, element by element.
+
+K1 records, bounding soundness, tile-culling decisions (exact outside a 1e-5 band), sort
+(bit-exact vs a stable sort of the emitted pairs), tile ranges, and images (max |err| <= 2e-3,
+>= 99.9% of pixels <= 5e-4 after ambiguity sets) on c1..c5 — full images where the oracle is
+fast, sampled pixels at the full BASELINE sizes in the configuration bench.py times.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+import paper_2504_12811_b200 as pkg  # noqa: E402
+from synth import scenes as S  # noqa: E402
+from tests.compare import compare  # noqa: E402
+from tests.helpers import one_gaussian, pinhole  # noqa: E402
+
+FI = {f: i for i, f in enumerate(O.G_FIELDS)}
+DI = {f: i for i, f in enumerate(pkg.DBG_FIELDS)}
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_12811_b200 import _build
+    _build.build()
+    return pkg.Renderer(0)
+
+
+def _img(R, cam):
+    rgb, T = R.render(cam)
+    torch.cuda.synchronize()
+    return torch.cat([rgb, T[None]], 0).permute(1, 2, 0).cpu().numpy().astype(np.float64)
+
+
+def _full_compare(R, scene, cam, **cfg):
+    R.load(scene)
+    img = _img(R, cam)
+    orc = O.Oracle(scene).set_view(cam)
+    yy, xx = np.mgrid[0:cam.height, 0:cam.width]
+    rep = compare(orc, img.reshape(-1, 4), xx.ravel(), yy.ravel())
+    return rep, img, orc
+
+
+def _sampled_compare(R, scene, cam, n_tiles=24, per_tile=48, seed=0, loaded=False):
+    if not loaded:
+        R.load(scene)
+    img = _img(R, cam)
+    rng = np.random.default_rng(seed)
+    tx = (cam.width + 15) // 16
+    ty = (cam.height + 15) // 16
+    tiles = rng.choice(tx * ty, n_tiles, replace=False)
+    px, py = [], []
+    for t in tiles:
+        x0, y0 = (t % tx) * 16, (t // tx) * 16
+        xs = rng.integers(x0, min(x0 + 16, cam.width), per_tile)
+        ys = rng.integers(y0, min(y0 + 16, cam.height), per_tile)
+        px.append(xs)
+        py.append(ys)
+    px = np.concatenate(px)
+    py = np.concatenate(py)
+    orc = O.Oracle(scene).set_view(cam)
+    rep = compare(orc, img[py, px], px, py)
+    return rep, img
+
+
+# ------------------------------------------------------------------ K1 records
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_k1_records_match_oracle(R, cfg):
+    scene, cams = S.make_config(cfg)
+    cam = cams[0]
+    R.load(scene)
+    R.set_camera(cam)
+    G = R.gaussian_records()
+    orc = O.Oracle(scene).set_view(cam)
+    Go = orc.gaussians()
+    tau_o = Go[:, FI["tau"]]
+    live = tau_o > 0
+    for f in ("vhat", "veff", "shat0", "shat1", "shat2", "A", "oA"):
+        a, b = G[live, DI[f]], Go[live, FI[f]]
+        fin = np.isfinite(b)
+        assert np.array_equal(np.isfinite(a), fin), f
+        np.testing.assert_allclose(a[fin], b[fin], rtol=1e-9, atol=1e-300, err_msg=f)
+    np.testing.assert_allclose(G[live, DI["tau"]], tau_o[live], rtol=1e-9, atol=1e-12)
+    # inside flag identical outside the 1e-5 band
+    margin = np.abs(Go[:, FI["inside_rho2"]] - tau_o) <= 1e-5 * np.maximum(1, np.abs(tau_o))
+    m = live & ~margin
+    np.testing.assert_array_equal(G[m, DI["inside"]], Go[m, FI["inside"]])
+    # colour (FP32 SH on the GPU) for Gaussians the GPU kept
+    vis = G[:, DI["visible"]] > 0
+    np.testing.assert_allclose(G[vis, DI["r"]:DI["b"] + 1], Go[vis, FI["r"]:FI["b"] + 1], atol=2e-6)
+    # whole-view cull: GPU visible <=> oracle min rho^2 over the screen frustum < tau
+    valid = live & (Go[:, FI["valid"]] > 0) & ~margin
+    idx = np.nonzero(valid)[0]
+    rect = np.tile([0.5, cam.width - 0.5, 0.5, cam.height - 0.5], (len(idx), 1))
+    mn = orc.frustum_min_rho2(idx, rect)
+    band = np.abs(mn - tau_o[idx]) <= 1e-5 * np.maximum(1, tau_o[idx])
+    want = mn < tau_o[idx]
+    got = G[idx, DI["visible"]] > 0
+    assert np.array_equal(got[~band], want[~band]), (np.sum(got[~band] != want[~band]), len(idx))
+    assert got.sum() > 0
+
+
+# ------------------------------------------------------------------ bounds + tile culling
+def _pairs_unsorted(R, cam):
+    R.set_camera(cam)
+    k, v = R.keys_vals(sorted_=False)
+    return k, v
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_bounds_and_tile_cull_match_oracle_qp(R, cfg):
+    scene, cams = S.make_config(cfg)
+    cam = cams[0]
+    R.load(scene)
+    R.set_camera(cam)
+    G = R.gaussian_records()
+    keys, vals = _pairs_unsorted(R, cam)
+    orc = O.Oracle(scene).set_view(cam)
+    tau = orc.gaussians()[:, FI["tau"]]
+    tx = (cam.width + 15) // 16
+    tile = (keys >> np.uint64(24)).astype(np.int64)
+    emitted = set(zip(vals.astype(np.int64).tolist(), tile.tolist()))
+    # every candidate tile of every visible Gaussian, decided by the oracle QP
+    gs, ts, rects = [], [], []
+    vis = np.nonzero(G[:, DI["visible"]] > 0)[0]
+    for g in vis:
+        x0, y0, x1, y1 = (int(G[g, DI[f]]) for f in ("tx0", "ty0", "tx1", "ty1"))
+        for yy in range(y0, y1 + 1):
+            for xx in range(x0, x1 + 1):
+                gs.append(g)
+                ts.append(yy * tx + xx)
+                rects.append((16 * xx + 0.5, min(16 * xx + 15.5, cam.width - 0.5),
+                              16 * yy + 0.5, min(16 * yy + 15.5, cam.height - 0.5)))
+    gs = np.asarray(gs)
+    ts = np.asarray(ts)
+    mn = orc.frustum_min_rho2(gs, np.asarray(rects))
+    band = np.abs(mn - tau[gs]) <= 1e-5 * np.maximum(1, tau[gs])
+    want = mn < tau[gs]
+    got = np.array([(g, t) in emitted for g, t in zip(gs.tolist(), ts.tolist())])
+    mism = (got != want) & ~band
+    assert not mism.any(), (mism.sum(), len(gs), gs[mism][:5], ts[mism][:5], mn[mism][:5], tau[gs][mism][:5])
+    assert len(emitted) == got.sum()          # nothing emitted outside the candidate rects
+    # bounding soundness: every oracle-contributing pixel lies in a kept tile of its Gaussian
+    rng = np.random.default_rng(1)
+    n_pix = 4096 if cfg == "c1" else 300
+    pxs = rng.integers(0, cam.width, n_pix)
+    pys = rng.integers(0, cam.height, n_pix)
+    for x, y in zip(pxs, pys):
+        c = orc.pixel_contribs(int(x), int(y))
+        t = (y // 16) * tx + x // 16
+        for row in c:
+            if row[O.C_FIELDS.index("included")] > 0.5 and not (int(row[O.C_FIELDS.index("flags")]) & O.F_CUTOFF):
+                assert (int(row[O.C_FIELDS.index("g")]), int(t)) in emitted, (x, y, row)
+
+
+# ------------------------------------------------------------------ sort + ranges
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_sort_bit_exact_and_ranges(R, cfg):
+    scene, cams = S.make_config(cfg)
+    cam = cams[0]
+    R.load(scene)
+    R.render(cam)
+    ks, vs = R.keys_vals(sorted_=True)
+    rng_ = R.ranges()
+    ku, vu = R.keys_vals(sorted_=False)
+    order = np.argsort(ku, kind="stable")
+    assert np.array_equal(ks, ku[order])
+    assert np.array_equal(vs, vu[order])
+    tiles = (ks >> np.uint64(24)).astype(np.int64)
+    n_tiles = rng_.shape[0]
+    starts = np.searchsorted(tiles, np.arange(n_tiles), "left")
+    ends = np.searchsorted(tiles, np.arange(n_tiles), "right")
+    empty = starts == ends
+    assert np.array_equal(rng_[~empty, 0], starts[~empty]) and np.array_equal(rng_[~empty, 1], ends[~empty])
+    assert np.all(rng_[empty, 0] == rng_[empty, 1])
+    if cfg == "c3":
+        st = R.stats()
+        assert st["pairs"] == len(ks) and st["candidates"] >= st["pairs"] > 1_000_000
+
+
+# ------------------------------------------------------------------ images
+def test_image_c1_full(R):
+    scene, cams = S.make_config("c1")
+    rep, img, _ = _full_compare(R, scene, cams[0])
+    assert rep["ok"], rep
+    assert img[..., 3].min() >= 0 and img[..., 3].max() <= 1
+
+
+def test_image_random_scene_full(R):
+    """Random-box scene with deep overlap (many window pops) and SH3, 128x96."""
+    scene = S.random_box_scene(17, 3000, 3, box=((-1.5, 1.5), (-1, 1), (1.0, 5.0)), scale_range=(0.01, 0.2))
+    cam = pinhole(W=128, H=96, f=90.0)
+    rep, img, _ = _full_compare(R, scene, cam)
+    assert rep["ok"], rep
+
+
+@pytest.mark.parametrize("view", [0, 37])
+def test_image_c2_full(R, view):
+    scene, cams = S.make_config("c2")
+    rep, _, _ = _full_compare(R, scene, cams[view])
+    assert rep["ok"], rep
+
+
+@pytest.mark.parametrize("cfg,view", [("c3", 0), ("c3", 100), ("c4wide", 3), ("c4zoomout", 10), ("c4inside", 49)])
+def test_image_full_size_sampled(R, cfg, view):
+    scene, cams = S.make_config(cfg)
+    rep, img = _sampled_compare(R, scene, cams[view], seed=view)
+    st = R.stats()
+    assert st["unresolved_pixels"] == 0, st
+    assert rep["ok"], (rep, st)
+
+
+def test_image_c5_sampled(R):
+    scene, cams = S.make_config("c5")
+    rep, img = _sampled_compare(R, scene, cams[0], n_tiles=16, per_tile=32)
+    assert rep["ok"], rep
+
+
+# ------------------------------------------------------------------ edge cases + invariants
+def test_determinism_and_window_independence(R):
+    scene, cams = S.make_config("c2")
+    cam = cams[5]
+    R.load(scene)
+    a = _img(R, cam)
+    b = _img(R, cam)
+    assert np.array_equal(a, b)
+    R.set_config(window_k=32)
+    c = _img(R, cam)
+    R.set_config(window_k=16, flags=pkg.AAA_FLAG_FORCE_FALLBACK)
+    d = _img(R, cam)
+    st = R.stats()
+    R.set_config(window_k=16, flags=0)
+    assert np.array_equal(a, c)
+    assert np.array_equal(a, d), np.abs(a - d).max()
+    assert st["overflow_tiles"] > 0
+
+
+def test_empty_scene_and_all_culled(R):
+    empty = S.Scene(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32), np.zeros((0, 4), np.float32),
+                    np.zeros(0, np.float32), np.zeros((0, 1, 3), np.float32), np.zeros(0, np.float32), 0)
+    R.set_config(background=(0.25, 0.5, 0.75))
+    R.load(empty)
+    img = _img(R, pinhole(W=40, H=24))
+    R.set_config(background=(0.0, 0.0, 0.0))
+    assert np.array_equal(img[..., :3], np.broadcast_to([0.25, 0.5, 0.75], (24, 40, 3)).astype(np.float32))
+    assert np.all(img[..., 3] == 1)
+    sc = one_gaussian((0, 0, -5.0), (0.1, 0.1, 0.1))  # behind the camera
+    R.load(sc)
+    img = _img(R, pinhole(W=40, H=24))
+    assert np.all(img[..., 3] == 1) and R.stats()["visible"] == 0
+
+
+def test_camera_inside_discard_and_straddler(R):
+    sc = S.c1_scene()
+    cam = S.c1_camera()
+    R.load(sc)
+    R.set_camera(cam)
+    G = R.gaussian_records()
+    assert G[61, DI["inside"]] == 1 and G[61, DI["visible"]] == 0      # (ii) camera inside
+    assert G[60, DI["visible"]] == 1 and G[60, DI["crossing"]] == 1    # (i) mean behind camera
+    assert G[63, DI["visible"]] == 1 and G[63, DI["crossing"]] == 1    # (iv) near straddler
+
+
+def test_host_pointer_render_and_bands(R):
+    scene, cams = S.make_config("c2")
+    cam = cams[11]
+    R.load(scene)
+    dev = _img(R, cam)
+    rgb = np.empty((3, cam.height, cam.width), np.float32)
+    T = np.empty((cam.height, cam.width), np.float32)
+    R.render_host(cam, rgb, T)
+    assert np.array_equal(rgb, dev[..., :3].transpose(2, 0, 1).astype(np.float32))
+    R.set_camera(cam)
+    rows = (cam.height + 15) // 16
+    cuts = [0, 7, 20, 33, rows]
+    parts = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        r, _ = R.render_tiles(a, b)
+        parts.append(r.cpu().numpy())
+    band = np.concatenate(parts, axis=1)
+    assert np.array_equal(band, dev[..., :3].transpose(2, 0, 1).astype(np.float32))
+
+
+def test_batch_equals_single(R):
+    scene, cams = S.make_config("c2")
+    R.load(scene)
+    sel = [cams[i] for i in (0, 9, 50)]
+    rgb, _ = R.render_batch(sel)
+    torch.cuda.synchronize()
+    for i, c in enumerate(sel):
+        assert np.array_equal(rgb[i].cpu().numpy(), _img(R, c)[..., :3].transpose(2, 0, 1).astype(np.float32))
+
+
+def test_fov_crop_equality_gpu(R):
+    """Large-FOV protocol: the centre crop of the 3x render equals the base render
+    within the image tolerance (FP32 evaluation at different p_ref)."""
+    scene, cams = S.make_config("c2")
+    base = cams[3]
+    wide = base.scaled(width=3 * base.width, height=3 * base.height, cx=base.cx + base.width,
+                       cy=base.cy + base.height)
+    R.load(scene)
+    a = _img(R, base)
+    b = _img(R, wide)[base.height:2 * base.height, base.width:2 * base.width]
+    err = np.abs(a[..., :3] - b[..., :3]).max(axis=2)
+    assert err.max() <= 2e-3 and (err <= 5e-4).mean() >= 0.999, (err.max(), (err <= 5e-4).mean())
+
+
+def test_invalid_inputs_rejected(R):
+    sc = one_gaussian((0, 0, 2.0), (0.1, -0.1, 0.1))
+    with pytest.raises(pkg.AaaError) as e:
+        R.load(sc)
+    assert e.value.first_bad == 0
+    bad_cam = pinhole()
+    bad_cam.world_to_view = np.diag([1.0, 1.0, -1.0, 1.0])
+    R.load(one_gaussian((0, 0, 2.0), (0.1, 0.1, 0.1)))
+    with pytest.raises(pkg.AaaError):
+        R.set_camera(bad_cam)
