@@ -56,7 +56,7 @@ typedef struct {
 /* Render configuration. Defaults from aaa_default_config():
  *   k = 0.3; tau_mode 0: tau = 2 ln(255 o A) per Gaussian (reading 1), tau_mode 1:
  *   tau = min(tau_fixed, 2 ln(255 o A)) with tau_fixed = 9; alpha_max = 0.99 (reading 2);
- *   T_eps = 1e-4 (reading 3); background black; window_k = 16 (per-pixel re-sort window,
+ *   T_eps = 1e-4 (reading 3); background black; window_k = 32 (per-pixel re-sort window,
  *   16 or 32); flags = 0. */
 typedef struct {
     float k;
@@ -86,12 +86,17 @@ typedef struct {
  * tiles whose per-pixel window overflowed (re-rendered by the quarter-tile K = 128 kernel),
  * quarters that overflowed again (re-rendered by the exact collect-and-sort kernel), pixels
  * whose contributions exceeded that kernel's capacity (0 unless the image is wrong),
- * Gaussians taking the near-plane-crossing cull path. ms[]: per-stage device times when
- * AAA_FLAG_TIMING is set (0 preprocess, 1 scan, 2 cull/emit, 3 sort, 4 ranges, 5 raster,
- * 6 fallback, 7 total). */
+ * Gaussians taking the near-plane-crossing cull path, pixel-Gaussian evaluations in the
+ * raster kernels, and the number of kernels this context has launched since creation.
+ * ms[]: mean per-view device time of each stage over the views rendered with AAA_FLAG_TIMING
+ * since the previous aaa_get_stats call (timed_views of them; the accumulation is reset by
+ * the call): 0 preprocess (K1), 1 scan (K2), 2 cull/emit (K3), 3 sort (K4), 4 ranges (K5),
+ * 5 raster (K6), 6 raster fallbacks (K6b + K6c), 7 host-sync gap after K2, 8 output copy
+ * (host outputs only), 9 total. */
 typedef struct {
     int64_t n, visible, candidates, pairs, overflow_tiles, overflow_quarters, unresolved_pixels, crossing;
-    float ms[8];
+    int64_t evaluations, launches, timed_views;
+    float ms[10];
 } aaa_stats;
 
 enum { AAA_FLAG_TIMING = 1u, AAA_FLAG_NO_TILE_CULL = 2u, AAA_FLAG_FORCE_FALLBACK = 4u };

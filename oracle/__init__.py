@@ -103,11 +103,13 @@ class Oracle:
             self._h = None
 
     def set_view(self, cam, **cfg):
+        # the C-ABI camera is float32; the oracle takes the same float32 values, promoted exactly
+        f32 = lambda v: float(np.float32(v))
         c = _Camera()
         c.width, c.height = int(cam.width), int(cam.height)
-        c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
-        c.world_to_view[:] = [float(v) for v in np.asarray(cam.world_to_view, dtype=np.float64).reshape(16)]
-        c.near_z = float(cam.near)
+        c.fx, c.fy, c.cx, c.cy = f32(cam.fx), f32(cam.fy), f32(cam.cx), f32(cam.cy)
+        c.world_to_view[:] = [f32(v) for v in np.asarray(cam.world_to_view, dtype=np.float64).reshape(16)]
+        c.near_z = f32(cam.near)
         d = default_config(**cfg)
         k = _Config()
         for f, _ in _Config._fields_:

@@ -45,7 +45,8 @@ class Gaussians(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("n", C.c_int64), ("visible", C.c_int64), ("candidates", C.c_int64), ("pairs", C.c_int64),
                 ("overflow_tiles", C.c_int64), ("overflow_quarters", C.c_int64),
-                ("unresolved_pixels", C.c_int64), ("crossing", C.c_int64), ("ms", C.c_float * 8)]
+                ("unresolved_pixels", C.c_int64), ("crossing", C.c_int64), ("evaluations", C.c_int64),
+                ("launches", C.c_int64), ("timed_views", C.c_int64), ("ms", C.c_float * 10)]
 
 
 _lib = None

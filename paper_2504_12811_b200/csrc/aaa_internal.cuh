@@ -78,7 +78,7 @@ struct ViewBufs {
 };
 
 constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_OVF1 = 4, CNT_OVF2 = 5,
-              CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16,
+              CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
               CNT_TOTAL = 32;
 
 // ---- launchers (each file implements its own) ----
@@ -120,5 +120,6 @@ struct RasterArgs {
     uint32_t* counters;
 };
 void launch_raster(const ViewParams& vp, const RasterArgs& ra, int window_k, cudaStream_t st);
+void launch_raster_fallback(const ViewParams& vp, const RasterArgs& ra, cudaStream_t st);
 
 }  // namespace aaa

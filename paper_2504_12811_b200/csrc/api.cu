@@ -42,10 +42,13 @@ struct aaa_ctx {
     uint32_t last_C = 0;
     int last_sorted = 0;
     int last_key_bits = 0;
-    float last_ms[8] = {0};
-    cudaEvent_t ev[9] = {};
-    bool events = false;
+    // per-view stage events (AAA_FLAG_TIMING): a pool reused across views, read at get_stats
+    std::vector<std::vector<cudaEvent_t>> ev_pool;
+    size_t ev_used = 0;
+    int64_t launches = 0;
 };
+
+constexpr int N_EV = 10;  // e0 K1 e1 K2 e2 [sync] e3 K3 e4 sort e5 ranges e6 K6 e7 K6b/c e8 [copy] e9
 
 namespace {
 
@@ -209,13 +212,18 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     if (s) return s;
     if (debug_k1 && !ctx->vb.dbg) CU(cudaMalloc(&ctx->vb.dbg, (size_t)(n > 0 ? n : 1) * AAA_DBG_GAUSS_FIELDS * sizeof(double)));
     CU(grow(ctx->vb.scan_state, ctx->scan_state_cap, scan_state_words(n) + 8));
-    const bool timing = (ctx->cfg.flags & AAA_FLAG_TIMING) != 0;
-    if (timing && !ctx->events) {
-        for (int i = 0; i < 9; i++) CU(cudaEventCreate(&ctx->ev[i]));
-        ctx->events = true;
+    const bool timing = (ctx->cfg.flags & AAA_FLAG_TIMING) != 0 && stop_after == 0;
+    cudaEvent_t* ev = nullptr;
+    if (timing) {
+        if (ctx->ev_used == ctx->ev_pool.size()) {
+            std::vector<cudaEvent_t> e(N_EV);
+            for (int i = 0; i < N_EV; i++) CU(cudaEventCreate(&e[i]));
+            ctx->ev_pool.push_back(e);
+        }
+        ev = ctx->ev_pool[ctx->ev_used++].data();
     }
     auto mark = [&](int i) {
-        if (timing) cudaEventRecord(ctx->ev[i], st);
+        if (ev) cudaEventRecord(ev[i], st);
     };
     CU(cudaMemsetAsync(ctx->vb.counters, 0, CNT_TOTAL * sizeof(uint32_t), st));
     size_t s2 = scan_state_words(n);
@@ -223,20 +231,23 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     mark(0);
     launch_preprocess(ctx->scene, vp, ctx->vb, debug_k1, st);
     mark(1);
+    if (n > 0) ctx->launches += 2;
     launch_scan(ctx->vb.counts, ctx->vb.offsets, n, &ctx->vb.counters[CNT_C], ctx->vb.scan_state,
                 &ctx->vb.counters[CNT_SCAN_TICKET], st);
     CU(cudaGetLastError());
+    mark(2);
     CU(cudaMemcpyAsync(ctx->h_counters, ctx->vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     const uint32_t C = ctx->h_counters[CNT_C];
     const int key_bits = DEPTH_KEY_BITS + bits_for((uint32_t)(vp.tiles_x * vp.tiles_y));
     s = ensure_pairs(ctx, C, sort_passes(key_bits));
     if (s) return s;
-    mark(2);
+    mark(3);
     size_t emit_words = (size_t)C / 2048 + 2;
     CU(cudaMemsetAsync(ctx->vb.scan_state, 0, emit_words * sizeof(uint32_t), st));
     launch_cull_emit(vp, ctx->vb, n, C, ctx->sb.keys[0], ctx->sb.vals[0], ctx->vb.scan_state, st);
-    mark(3);
+    mark(4);
+    if (C > 0) ctx->launches += 1;
     ctx->last_vp = vp;
     ctx->last_C = C;
     ctx->last_key_bits = key_bits;
@@ -247,9 +258,10 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     }
     int sorted = launch_sort(ctx->sb, &ctx->vb.counters[CNT_P], C, key_bits, st);
     ctx->last_sorted = sorted;
-    mark(4);
-    launch_ranges(ctx->sb.keys[sorted], &ctx->vb.counters[CNT_P], C, ctx->ranges, vp.tiles_x * vp.tiles_y, st);
     mark(5);
+    launch_ranges(ctx->sb.keys[sorted], &ctx->vb.counters[CNT_P], C, ctx->ranges, vp.tiles_x * vp.tiles_y, st);
+    mark(6);
+    if (C > 0) ctx->launches += 3 + sort_passes(key_bits);
     RasterArgs ra{};
     ra.keys = ctx->sb.keys[sorted];
     ra.vals = ctx->sb.vals[sorted];
@@ -264,7 +276,10 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.ovf_list2 = ctx->ovf2;
     ra.counters = ctx->vb.counters;
     launch_raster(vp, ra, ctx->cfg.window_k, st);
-    mark(6);
+    mark(7);
+    launch_raster_fallback(vp, ra, st);
+    mark(8);
+    if (vp.tile_row_end > vp.tile_row_begin) ctx->launches += 3;
     CU(cudaGetLastError());
     return AAA_OK;
 }
@@ -301,12 +316,8 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
         if (s) return s;
         if (!dev_rgb) CU(cudaMemcpyAsync(rgb + 3 * plane * v, r, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
         if (T && !dev_T) CU(cudaMemcpyAsync(T + plane * v, t, plane * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-        if (ctx->cfg.flags & AAA_FLAG_TIMING) {
-            CU(cudaEventSynchronize(ctx->ev[6]));
-            for (int i = 0; i < 6; i++) cudaEventElapsedTime(&ctx->last_ms[i], ctx->ev[i], ctx->ev[i + 1]);
-            ctx->last_ms[7] = 0;
-            for (int i = 0; i < 6; i++) ctx->last_ms[7] += ctx->last_ms[i];
-        }
+        if ((ctx->cfg.flags & AAA_FLAG_TIMING) && ctx->ev_used > 0)
+            CU(cudaEventRecord(ctx->ev_pool[ctx->ev_used - 1][9], ctx->stream));
     }
     if (!dev_rgb || !dev_T) CU(cudaStreamSynchronize(ctx->stream));
     return AAA_OK;
@@ -351,8 +362,8 @@ void aaa_destroy(aaa_ctx* ctx) {
     cudaFree(ctx->sb.hist); cudaFree(ctx->sb.state); cudaFree(ctx->sb.tickets);
     cudaFree(ctx->ranges); cudaFree(ctx->ovf1); cudaFree(ctx->ovf2); cudaFree(ctx->d_out);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
-    if (ctx->events)
-        for (int i = 0; i < 9; i++) cudaEventDestroy(ctx->ev[i]);
+    for (auto& e : ctx->ev_pool)
+        for (auto x : e) cudaEventDestroy(x);
     delete ctx;
 }
 
@@ -370,7 +381,7 @@ aaa_status aaa_default_config(aaa_config* c) {
     c->alpha_max = 0.99f;
     c->T_eps = 1e-4f;
     c->background[0] = c->background[1] = c->background[2] = 0.f;
-    c->window_k = 16;
+    c->window_k = 32;
     c->flags = 0;
     return AAA_OK;
 }
@@ -515,7 +526,25 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     out->overflow_quarters = h[CNT_OVF2];
     out->unresolved_pixels = h[CNT_UNRESOLVED];
     out->crossing = h[CNT_CROSS];
-    for (int i = 0; i < 8; i++) out->ms[i] = ctx->last_ms[i];
+    out->evaluations = h[CNT_EVAL];
+    out->launches = ctx->launches;
+    // per-stage means over the timed views since the previous call
+    // stages: K1, K2, K3, sort, ranges, K6, K6b+K6c, host-sync gap, output copy, total
+    const int a[10] = {0, 1, 3, 4, 5, 6, 7, 2, 8, 0}, b[10] = {1, 2, 4, 5, 6, 7, 8, 3, 9, 9};
+    double acc[10] = {0};
+    int64_t nv = 0;
+    for (size_t v = 0; v < ctx->ev_used; v++) {
+        cudaEvent_t* e = ctx->ev_pool[v].data();
+        float t[10];
+        bool ok = true;
+        for (int i = 0; i < 10; i++) ok = ok && cudaEventElapsedTime(&t[i], e[a[i]], e[b[i]]) == cudaSuccess;
+        if (!ok) { cudaGetLastError(); continue; }
+        for (int i = 0; i < 10; i++) acc[i] += t[i];
+        nv++;
+    }
+    ctx->ev_used = 0;
+    out->timed_views = nv;
+    for (int i = 0; i < 10; i++) out->ms[i] = nv ? (float)(acc[i] / nv) : 0.f;
     return AAA_OK;
 }
 

@@ -1,0 +1,125 @@
+"""Multi-GPU partitioner (L6): one process per GPU; work is split by camera (view batches) or,
+for one huge frame, by screen-space tile-row bands. NCCL (torch.distributed) is used only to
+broadcast the Gaussian set from rank 0 and to gather images — rendering itself exchanges
+nothing. Pure host logic lives in plain functions so it can be tested on CPU with
+the gloo backend.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SCENE_FIELDS = ("means", "scales", "quats", "opacities", "sh", "v_train")
+
+
+def view_block(n_views: int, rank: int, world: int, per_rank: int) -> list[int]:
+    """Views of `rank` for one step: per_rank views interleaved along the camera path
+    (view k*stride + rank, stride = max(8, world)), so every rank sees the same mix of near and
+    far views and the union over 8 ranks of 25 views is the whole 200-view orbit."""
+    stride = max(8, world)
+    return [(k * stride + rank) % n_views for k in range(per_rank)]
+
+
+def view_shard(n_views: int, rank: int, world: int) -> list[int]:
+    """Strong-scaling shard of a fixed batch: round-robin (balances cost along the path)."""
+    return list(range(rank, n_views, world))
+
+
+def band_split(row_costs, world: int) -> list[tuple[int, int]]:
+    """Split tile rows [0, R) into `world` contiguous bands of near-equal cost (prefix-sum
+    cut points); every band gets >= 1 row when R >= world. Identical on every rank."""
+    c = np.asarray(row_costs, dtype=np.float64)
+    R = c.shape[0]
+    if world <= 1 or R == 0:
+        return [(0, R)]
+    pref = np.concatenate([[0.0], np.cumsum(c + 1e-9)])   # +eps: empty rows still count a little
+    total = pref[-1]
+    cuts = [0]
+    for k in range(1, world):
+        target = total * k / world
+        r = int(np.searchsorted(pref, target))
+        lo = cuts[-1] + 1
+        hi = R - (world - k)
+        cuts.append(int(min(max(r, lo), hi)) if R >= world else min(k, R))
+    cuts.append(R)
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+def scene_to_tensors(scene, device):
+    import torch
+    t = {f: torch.from_numpy(np.ascontiguousarray(getattr(scene, f), dtype=np.float32)).to(device)
+         for f in SCENE_FIELDS}
+    t["sh_degree"] = scene.sh_degree
+    return t
+
+
+def broadcast_scene(scene_or_none, rank: int, world: int, device, src: int = 0):
+    """Broadcast the Gaussian SoA from `src` to every rank (NCCL on GPUs, gloo on CPU).
+    Returns a dict of tensors on `device` (+ 'sh_degree')."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return scene_to_tensors(scene_or_none, device)
+    if rank == src:
+        t = scene_to_tensors(scene_or_none, device)
+        meta = torch.tensor([t["means"].shape[0], t["sh_degree"]], dtype=torch.int64, device=device)
+    else:
+        meta = torch.zeros(2, dtype=torch.int64, device=device)
+    dist.broadcast(meta, src)
+    n, deg = int(meta[0]), int(meta[1])
+    K = (deg + 1) ** 2
+    shapes = {"means": (n, 3), "scales": (n, 3), "quats": (n, 4), "opacities": (n,), "sh": (n, K, 3),
+              "v_train": (n,)}
+    if rank != src:
+        t = {f: torch.empty(shapes[f], dtype=torch.float32, device=device) for f in SCENE_FIELDS}
+        t["sh_degree"] = deg
+    for f in SCENE_FIELDS:
+        dist.broadcast(t[f], src)
+    return t
+
+
+def load_scene_broadcast(config: str, rank: int, world: int, device):
+    """Rank 0 generates the seeded scene of `config`; NCCL broadcasts it. Cameras are cheap and
+    deterministic, so every rank builds them locally."""
+    from synth import scenes as S
+    if rank == 0 or world <= 1:
+        scene, cams = S.make_config(config)
+    else:
+        scene = None
+        cams = _cameras_only(config)
+    t = broadcast_scene(scene, rank, world, device)
+    return t, cams, t["sh_degree"]
+
+
+def _cameras_only(config: str):
+    from synth import scenes as S
+    if config == "c1":
+        return [S.c1_camera()]
+    if config == "c2":
+        return S.c2_cameras()
+    if config == "c3":
+        return S.c3_cameras()
+    if config.startswith("c4"):
+        return S.c4_cameras(config[2:])
+    if config == "c5":
+        return [S.c5_camera()]
+    raise ValueError(config)
+
+
+def gather_bands(band_rgb, bands, width: int, height: int, rank: int, world: int, dst: int = 0):
+    """Assemble tile-row bands (3 x band_h x W each) into the full 3 x H x W frame on `dst`
+    with one NCCL all-gather of equal-size padded bands."""
+    import torch
+    import torch.distributed as dist
+    max_h = max(min(16 * b, height) - 16 * a for a, b in bands)
+    pad = torch.zeros((3, max_h, width), dtype=band_rgb.dtype, device=band_rgb.device)
+    pad[:, : band_rgb.shape[1]] = band_rgb
+    out = torch.empty((world * 3, max_h, width), dtype=band_rgb.dtype, device=band_rgb.device)
+    dist.all_gather_into_tensor(out, pad)
+    out = out.view(world, 3, max_h, width)
+    if rank != dst:
+        return None
+    parts = []
+    for r, (a, b) in enumerate(bands):
+        h = min(16 * b, height) - 16 * a
+        parts.append(out[r, :, :h])
+    return torch.cat(parts, dim=1)

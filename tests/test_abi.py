@@ -49,7 +49,7 @@ def test_default_config_without_gpu(built):
     import paper_2504_12811_b200 as pkg
     cfg = pkg.Config()
     assert pkg.lib().aaa_default_config(C.byref(cfg)) == 0
-    assert abs(cfg.k - 0.3) < 1e-7 and abs(cfg.alpha_max - 0.99) < 1e-7 and cfg.window_k == 16
+    assert abs(cfg.k - 0.3) < 1e-7 and abs(cfg.alpha_max - 0.99) < 1e-7 and cfg.window_k == 32
 
 
 def test_no_cpu_fallback_in_product_path():

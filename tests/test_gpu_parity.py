@@ -83,8 +83,9 @@ def test_k1_records_match_oracle(R, cfg):
         a, b = G[live, DI[f]], Go[live, FI[f]]
         fin = np.isfinite(b)
         assert np.array_equal(np.isfinite(a), fin), f
-        np.testing.assert_allclose(a[fin], b[fin], rtol=1e-9, atol=1e-300, err_msg=f)
-    np.testing.assert_allclose(G[live, DI["tau"]], tau_o[live], rtol=1e-9, atol=1e-12)
+        # 1e-7: the C-ABI carries k as float32 (0.3f = 0.3 + 1.2e-8); everything else is FP64
+        np.testing.assert_allclose(a[fin], b[fin], rtol=1e-7, atol=1e-300, err_msg=f)
+    np.testing.assert_allclose(G[live, DI["tau"]], tau_o[live], rtol=1e-7, atol=1e-9)
     # inside flag identical outside the 1e-5 band
     margin = np.abs(Go[:, FI["inside_rho2"]] - tau_o) <= 1e-5 * np.maximum(1, np.abs(tau_o))
     m = live & ~margin
@@ -228,12 +229,12 @@ def test_determinism_and_window_independence(R):
     a = _img(R, cam)
     b = _img(R, cam)
     assert np.array_equal(a, b)
-    R.set_config(window_k=32)
+    R.set_config(window_k=16)
     c = _img(R, cam)
-    R.set_config(window_k=16, flags=pkg.AAA_FLAG_FORCE_FALLBACK)
+    R.set_config(window_k=32, flags=pkg.AAA_FLAG_FORCE_FALLBACK)
     d = _img(R, cam)
     st = R.stats()
-    R.set_config(window_k=16, flags=0)
+    R.set_config(window_k=32, flags=0)
     assert np.array_equal(a, c)
     assert np.array_equal(a, d), np.abs(a - d).max()
     assert st["overflow_tiles"] > 0
