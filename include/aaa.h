@@ -83,18 +83,17 @@ typedef struct {
 
 /* Counters of the last rendered view: N loaded, V visible after preprocessing,
  * C candidate (Gaussian, tile) pairs from the bounds, P pairs kept by 3D tile culling,
- * tiles whose per-pixel window overflowed (re-rendered by the quarter-tile K = 128 kernel),
- * quarters that overflowed again (re-rendered by the exact collect-and-sort kernel), pixels
- * whose contributions exceeded that kernel's capacity (0 unless the image is wrong),
+ * pixels whose K6 per-pixel window filled (their exact state is spilled and finished by the
+ * K6s kernel), pixels K6s could not resolve exactly (0 unless the image is wrong),
  * Gaussians taking the near-plane-crossing cull path, pixel-Gaussian evaluations in the
  * raster kernels, and the number of kernels this context has launched since creation.
  * ms[]: mean per-view device time of each stage over the views rendered with AAA_FLAG_TIMING
  * since the previous aaa_get_stats call (timed_views of them; the accumulation is reset by
  * the call): 0 preprocess (K1), 1 scan (K2), 2 cull/emit (K3), 3 sort (K4), 4 ranges (K5),
- * 5 raster (K6), 6 raster fallbacks (K6b + K6c), 7 host-sync gap after K2, 8 output copy
+ * 5 raster (K6), 6 spilled-pixel continuation (K6s), 7 host-sync gap after K2, 8 output copy
  * (host outputs only), 9 total. */
 typedef struct {
-    int64_t n, visible, candidates, pairs, overflow_tiles, overflow_quarters, unresolved_pixels, crossing;
+    int64_t n, visible, candidates, pairs, spilled_pixels, unresolved_pixels, crossing;
     int64_t evaluations, launches, timed_views;
     float ms[10];
 } aaa_stats;
@@ -109,7 +108,9 @@ enum {
     AAA_DBG_KEYS_UNSORTED = 3, /* P uint64 keys in emission order                         */
     AAA_DBG_VALS_UNSORTED = 4, /* P uint32 values in emission order                       */
     AAA_DBG_RANGES = 5, /* tiles x 2 uint32 [start, end)                                     */
-    AAA_DBG_OVERFLOW = 6 /* overflow tile ids, uint32                                        */
+    AAA_DBG_SPILL = 6,   /* spilled pixels: 8 x 32-bit (pixel, list pos, count, T, r, g, b, 0) */
+    AAA_DBG_RASTER = 7,  /* N x 28 float32 raster records of the last view (K6 inputs)         */
+    AAA_DBG_COLOR = 8    /* N x 4 float32 colours of the last view                              */
 };
 /* per-Gaussian debug record: v_hat, v_eff, s_hat[3], A, oA, tau, valid(after inside test),
  * inside, inside_rho2, colour[3], visible (kept by the whole-view cull), crossing,

@@ -8,7 +8,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libaaa.so"
 
 AAA_FLAG_TIMING, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_FORCE_FALLBACK = 1, 2, 4
 (AAA_DBG_GAUSS, AAA_DBG_KEYS, AAA_DBG_VALS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_VALS_UNSORTED, AAA_DBG_RANGES,
- AAA_DBG_OVERFLOW) = range(7)
+ AAA_DBG_SPILL, AAA_DBG_RASTER, AAA_DBG_COLOR) = range(9)
 AAA_DBG_GAUSS_FIELDS = 26
 
 EXPORTED_SYMBOLS = ["aaa_version", "aaa_create", "aaa_destroy", "aaa_set_stream", "aaa_default_config",
@@ -44,8 +44,7 @@ class Gaussians(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("n", C.c_int64), ("visible", C.c_int64), ("candidates", C.c_int64), ("pairs", C.c_int64),
-                ("overflow_tiles", C.c_int64), ("overflow_quarters", C.c_int64),
-                ("unresolved_pixels", C.c_int64), ("crossing", C.c_int64), ("evaluations", C.c_int64),
+                ("spilled_pixels", C.c_int64), ("unresolved_pixels", C.c_int64), ("crossing", C.c_int64), ("evaluations", C.c_int64),
                 ("launches", C.c_int64), ("timed_views", C.c_int64), ("ms", C.c_float * 10)]
 
 

@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for s in SOURCES:
         o = objdir / (Path(s).stem + ".o")
         objs.append(o)
-        cmd = [NVCC, *FLAGS, "-c", str(CSRC / s), "-o", str(o)]
+        cmd = [NVCC, *FLAGS, *os.environ.get("AAA_NVCC_FLAGS", "").split(), "-c", str(CSRC / s), "-o", str(o)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -14,6 +14,11 @@ constexpr int DEPTH_KEY_SHIFT = 7;
 constexpr int RASTER_REC_F4 = 7;        // raster record: 7 float4 = 112 B
 constexpr float ANGLE_EPS = 1e-4f;      // Eq. 17 epsilon (reading 17)
 constexpr double ZKEY_PAD = 1e-5;       // relative downward pad of the depth key (reading 23)
+// pair value: Gaussian index (low 24 bits) | 8-bit mask of the 8x4 warp sub-tiles it may touch
+constexpr int VAL_INDEX_BITS = 24;
+constexpr uint32_t VAL_INDEX_MASK = (1u << VAL_INDEX_BITS) - 1u;
+constexpr uint32_t SUBTILE_ALL = 0xFFu;
+constexpr int64_t MAX_GAUSSIANS = 1ll << VAL_INDEX_BITS;
 
 // Per-view constants passed by value to every kernel (camera in double for the FP64 geometry).
 struct ViewParams {
@@ -71,13 +76,13 @@ struct ViewBufs {
     CrossRec* cross;      // n (worst case)
     double* dbg;          // n * AAA_DBG_GAUSS_FIELDS (only when debugging)
     // device counters: [0] visible, [1] crossing slots, [2] C total, [3] P pairs,
-    // [4] overflow tiles (K6), [5] overflow quarters (K6b), [6] unresolved pixels (K6c),
+    // [4] spilled pixels (K6 windows that filled), [5] K6s ticket, [6] unresolved pixels,
     // [7] tickets (scratch), [8..15] sort tickets, [16] K3 ticket
     uint32_t* counters;
     uint32_t* scan_state; // decoupled look-back state for the scan / emit / sort
 };
 
-constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_OVF1 = 4, CNT_OVF2 = 5,
+constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_SPILL = 4, CNT_SPILL_TICKET = 5,
               CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
               CNT_TOTAL = 32;
 
@@ -105,6 +110,12 @@ size_t sort_state_words(uint32_t cap, int passes);
 int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st);
 void launch_ranges(const uint64_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles,
                    cudaStream_t st);
+// exact state of a pixel whose K6 window filled: K6s resumes it at list position `pos`
+struct SpillHdr {
+    uint32_t pixel, pos, cnt;
+    float T, Cr, Cg, Cb;
+    uint32_t pad;
+};
 struct RasterArgs {
     const uint64_t* keys;
     const uint32_t* vals;
@@ -115,8 +126,10 @@ struct RasterArgs {
     float* out_T;         // out_h x W (nullable)
     int out_row0;         // first image row stored in out (band renders)
     int out_h;
-    uint32_t* ovf_list1;  // tiles that overflowed K = window_k
-    uint32_t* ovf_list2;  // (tile, quarter) that overflowed K6b
+    SpillHdr* spill_hdr;  // spilled pixel states (K6 -> K6s)
+    float4* spill_e;      // spill_k window entries per spilled pixel: (z, alpha, g bits, 0)
+    uint32_t spill_cap;
+    uint32_t spill_k;
     uint32_t* counters;
 };
 void launch_raster(const ViewParams& vp, const RasterArgs& ra, int window_k, cudaStream_t st);

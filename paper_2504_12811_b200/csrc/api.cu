@@ -30,9 +30,10 @@ struct aaa_ctx {
     size_t sort_state_cap = 0;
     uint2* ranges = nullptr;
     int ranges_cap = 0;
-    uint32_t* ovf1 = nullptr;
-    uint32_t* ovf2 = nullptr;
-    int ovf_cap = 0;
+    SpillHdr* spill_hdr = nullptr;
+    float4* spill_e = nullptr;
+    size_t spill_cap = 0;
+    int spill_k = 0;
     uint32_t* h_counters = nullptr;  // pinned
     float* d_out = nullptr;
     size_t d_out_cap = 0;
@@ -164,12 +165,29 @@ aaa_status ensure_view_bufs(aaa_ctx* ctx, int64_t n) {
 
 aaa_status ensure_tiles(aaa_ctx* ctx, int n_tiles) {
     if (n_tiles <= ctx->ranges_cap) return AAA_OK;
-    cudaFree(ctx->ranges); cudaFree(ctx->ovf1); cudaFree(ctx->ovf2);
-    ctx->ranges = nullptr; ctx->ovf1 = ctx->ovf2 = nullptr;
+    cudaFree(ctx->ranges);
+    ctx->ranges = nullptr;
     CU(cudaMalloc(&ctx->ranges, (size_t)n_tiles * sizeof(uint2)));
-    CU(cudaMalloc(&ctx->ovf1, (size_t)n_tiles * sizeof(uint32_t)));
-    CU(cudaMalloc(&ctx->ovf2, (size_t)n_tiles * 4 * sizeof(uint32_t)));
     ctx->ranges_cap = n_tiles;
+    return AAA_OK;
+}
+
+// Spill slots for pixels whose K6 window fills: one per pixel up to 4M per view (beyond that a
+// pixel is counted as unresolved by aaa_get_stats), each holding the window's K entries.
+constexpr size_t MAX_SPILL = (size_t)1 << 22;
+
+aaa_status ensure_spill(aaa_ctx* ctx, size_t pixels, int k) {
+    size_t cap = std::min(pixels, MAX_SPILL);
+    if (cap <= ctx->spill_cap && k <= ctx->spill_k) return AAA_OK;
+    cudaFree(ctx->spill_hdr);
+    cudaFree(ctx->spill_e);
+    ctx->spill_hdr = nullptr;
+    ctx->spill_e = nullptr;
+    ctx->spill_cap = 0;
+    CU(cudaMalloc(&ctx->spill_hdr, cap * sizeof(SpillHdr)));
+    CU(cudaMalloc(&ctx->spill_e, cap * (size_t)k * sizeof(float4)));
+    ctx->spill_cap = cap;
+    ctx->spill_k = k;
     return AAA_OK;
 }
 
@@ -272,8 +290,13 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.out_T = T;
     ra.out_row0 = row_begin * TILE;
     ra.out_h = std::min(row_end * TILE, cam.height) - row_begin * TILE;
-    ra.ovf_list1 = ctx->ovf1;
-    ra.ovf_list2 = ctx->ovf2;
+    const int win_k = (ctx->cfg.flags & AAA_FLAG_FORCE_FALLBACK) ? 1 : ctx->cfg.window_k;
+    s = ensure_spill(ctx, (size_t)cam.width * cam.height, std::max(win_k, ctx->spill_k));
+    if (s) return s;
+    ra.spill_hdr = ctx->spill_hdr;
+    ra.spill_e = ctx->spill_e;
+    ra.spill_cap = (uint32_t)ctx->spill_cap;
+    ra.spill_k = (uint32_t)ctx->spill_k;
     ra.counters = ctx->vb.counters;
     launch_raster(vp, ra, ctx->cfg.window_k, st);
     mark(7);
@@ -360,7 +383,7 @@ void aaa_destroy(aaa_ctx* ctx) {
     cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
     for (int i = 0; i < 2; i++) { cudaFree(ctx->sb.keys[i]); cudaFree(ctx->sb.vals[i]); }
     cudaFree(ctx->sb.hist); cudaFree(ctx->sb.state); cudaFree(ctx->sb.tickets);
-    cudaFree(ctx->ranges); cudaFree(ctx->ovf1); cudaFree(ctx->ovf2); cudaFree(ctx->d_out);
+    cudaFree(ctx->ranges); cudaFree(ctx->spill_hdr); cudaFree(ctx->spill_e); cudaFree(ctx->d_out);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev_pool)
         for (auto x : e) cudaEventDestroy(x);
@@ -403,7 +426,7 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
         return fail(ctx, AAA_ERR_INVALID_ARG, "n must be >= 0 and sh_degree in 0..3");
     if (g->n > 0 && (!g->means || !g->scales || !g->quats || !g->opacities || !g->sh || !g->v_train))
         return fail(ctx, AAA_ERR_INVALID_ARG, "null scene array");
-    if (g->n >= (1ll << 31)) return fail(ctx, AAA_ERR_INVALID_ARG, "n too large (< 2^31)");
+    if (g->n > MAX_GAUSSIANS) return fail(ctx, AAA_ERR_INVALID_ARG, "n too large (<= 2^24 Gaussians per context)");
     CU(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
     SceneDev& s = ctx->scene;
@@ -522,8 +545,7 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     out->visible = h[CNT_VISIBLE];
     out->candidates = h[CNT_C];
     out->pairs = h[CNT_P];
-    out->overflow_tiles = h[CNT_OVF1];
-    out->overflow_quarters = h[CNT_OVF2];
+    out->spilled_pixels = h[CNT_SPILL];
     out->unresolved_pixels = h[CNT_UNRESOLVED];
     out->crossing = h[CNT_CROSS];
     out->evaluations = h[CNT_EVAL];
@@ -568,10 +590,13 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
     } else if (what == AAA_DBG_KEYS_UNSORTED || what == AAA_DBG_VALS_UNSORTED) {
         s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, false, 1);
         src = what == AAA_DBG_KEYS_UNSORTED ? (const void*)ctx->sb.keys[0] : (const void*)ctx->sb.vals[0];
-    } else if (what == AAA_DBG_KEYS || what == AAA_DBG_VALS || what == AAA_DBG_RANGES || what == AAA_DBG_OVERFLOW) {
+    } else if (what == AAA_DBG_KEYS || what == AAA_DBG_VALS || what == AAA_DBG_RANGES || what == AAA_DBG_SPILL) {
         src = what == AAA_DBG_KEYS ? (const void*)ctx->sb.keys[ctx->last_sorted]
             : what == AAA_DBG_VALS ? (const void*)ctx->sb.vals[ctx->last_sorted]
-            : what == AAA_DBG_RANGES ? (const void*)ctx->ranges : (const void*)ctx->ovf1;
+            : what == AAA_DBG_RANGES ? (const void*)ctx->ranges : (const void*)ctx->spill_hdr;
+    } else if (what == AAA_DBG_RASTER || what == AAA_DBG_COLOR) {
+        src = what == AAA_DBG_RASTER ? (const void*)ctx->vb.raster : (const void*)ctx->vb.color;
+        bytes = (size_t)ctx->scene.n * (what == AAA_DBG_RASTER ? RASTER_REC_F4 : 1) * sizeof(float4);
     } else {
         return fail(ctx, AAA_ERR_INVALID_ARG, "unknown debug buffer");
     }
@@ -582,7 +607,7 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
     if (what == AAA_DBG_KEYS || what == AAA_DBG_KEYS_UNSORTED) bytes = (size_t)h[CNT_P] * 8;
     if (what == AAA_DBG_VALS || what == AAA_DBG_VALS_UNSORTED) bytes = (size_t)h[CNT_P] * 4;
     if (what == AAA_DBG_RANGES) bytes = (size_t)ctx->last_vp.tiles_x * ctx->last_vp.tiles_y * sizeof(uint2);
-    if (what == AAA_DBG_OVERFLOW) bytes = (size_t)h[CNT_OVF1] * 4;
+    if (what == AAA_DBG_SPILL) bytes = (size_t)std::min((size_t)h[CNT_SPILL], ctx->spill_cap) * sizeof(SpillHdr);
     *len = bytes;
     if (bytes > cap) return fail(ctx, AAA_ERR_INVALID_ARG, "debug buffer too small");
     if (bytes && src) CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));

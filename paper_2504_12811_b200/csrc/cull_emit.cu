@@ -75,11 +75,25 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
         double x0 = TILE * tx + 0.5, x1 = fmin(TILE * tx + TILE - 0.5, vp.width - 0.5);
         double y0 = TILE * ty + 0.5, y1 = fmin(TILE * ty + TILE - 0.5, vp.height - 0.5);
         bool keep;
+        uint32_t sub = SUBTILE_ALL;
         if (no_cull) {
             keep = true;
         } else if (r.cross_slot < 0) {
             double px = r.pref_x, py = r.pref_y;
             keep = quad_box_min(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, x0 - px, x1 - px, y0 - py, y1 - py) < 0.0;
+            if (keep) {
+                // the same exact test on each 8x4 warp sub-tile (pixel-centre rects): the raster
+                // kernels skip the Gaussian on sub-tiles whose bit is clear ("repeated culling")
+                sub = 0;
+#pragma unroll
+                for (int s = 0; s < 8; s++) {
+                    double sx0 = TILE * tx + 8 * (s & 1) + 0.5, sy0 = TILE * ty + 4 * (s >> 1) + 0.5;
+                    if (sx0 > vp.width - 0.5 || sy0 > vp.height - 0.5) continue;
+                    double sx1 = fmin(sx0 + 7.0, vp.width - 0.5), sy1 = fmin(sy0 + 3.0, vp.height - 0.5);
+                    if (quad_box_min(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, sx0 - px, sx1 - px, sy0 - py, sy1 - py) < 0.0)
+                        sub |= 1u << s;
+                }
+            }
         } else {
             const CrossRec& cr = cross[r.cross_slot];
             keep = frustum_qp_min(cr.M, cr.muv, vp.fx, vp.fy, vp.cx, vp.cy, vp.near_z, x0, x1, y0, y1) < cr.tau;
@@ -87,7 +101,7 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
         if (keep) {
             uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
             key[k] = ((uint64_t)tile << DEPTH_KEY_BITS) | r.zkey;
-            val[k] = (uint32_t)g;
+            val[k] = (uint32_t)g | (sub << VAL_INDEX_BITS);
             keep_mask |= 1u << k;
             nkeep++;
         }

@@ -23,6 +23,8 @@ __device__ __forceinline__ void mat3_mul(const double* A, const double* B, doubl
 // rotation matrix (row-major) of a normalised (w,x,y,z) quaternion (Eq. 3 R)
 __device__ __forceinline__ void quat_to_rot(float4 q, double* R) {
     double w = q.x, x = q.y, y = q.z, z = q.w;
+    double inv = 1.0 / sqrt(w * w + x * x + y * y + z * z);  // normalise in FP64
+    w *= inv; x *= inv; y *= inv; z *= inv;
     R[0] = 1.0 - 2.0 * (y * y + z * z); R[1] = 2.0 * (x * y - w * z);       R[2] = 2.0 * (x * z + w * y);
     R[3] = 2.0 * (x * y + w * z);       R[4] = 1.0 - 2.0 * (x * x + z * z); R[5] = 2.0 * (y * z - w * x);
     R[6] = 2.0 * (x * z - w * y);       R[7] = 2.0 * (y * z + w * x);       R[8] = 1.0 - 2.0 * (x * x + y * y);

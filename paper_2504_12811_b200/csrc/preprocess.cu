@@ -42,8 +42,8 @@ __global__ void k_load_pack(int64_t n, int deg, const float* __restrict__ means,
     if (!ok) atomicMin(first_bad, (unsigned long long)g);
     geomA[g] = make_float4(mx, my, mz, o);
     geomB[g] = make_float4(sx, sy, sz, v);
-    geomC[g] = ok ? make_float4((float)(qw / qn), (float)(qx / qn), (float)(qy / qn), (float)(qz / qn))
-                  : make_float4(1.f, 0.f, 0.f, 0.f);
+    // raw quaternion: K1 normalises it in FP64 (a f32-rounded unit quaternion would perturb R by ~1e-7)
+    geomC[g] = ok ? make_float4(qw, qx, qy, qz) : make_float4(1.f, 0.f, 0.f, 0.f);
     for (int c = 0; c < chunks; c++) {
         float e[4];
         for (int j = 0; j < 4; j++) e[j] = (4 * c + j < nf) ? s[4 * c + j] : 0.f;
@@ -106,7 +106,6 @@ __device__ __forceinline__ void sh_color(const float4* __restrict__ sh, int64_t 
 // Returns false when no front-facing ray of this plane family meets the ellipsoid.
 __device__ bool axis_bounds(double s_ii, double s_i3, double s33, double disc, double mu_i, double mu_z, double f,
                             double c, double& lo, double& hi) {
-    const double PI = CUDART_PI;
     if (!(disc >= 0.0)) {  // the ellipsoid meets the plane family's axis: full axis
         lo = -CUDART_INF;
         hi = CUDART_INF;
@@ -114,36 +113,37 @@ __device__ bool axis_bounds(double s_ii, double s_i3, double s33, double disc, d
     }
     double sq = sqrt(disc);
     double num = s_i3 + copysign(sq, s_i3);
-    if (num == 0.0) {
+    double mn = sqrt(mu_i * mu_i + mu_z * mu_z);
+    if (num == 0.0 || mn == 0.0) {
         lo = -CUDART_INF;
         hi = CUDART_INF;
         return true;
     }
-    double r1 = atan2(num, s33);   // tan r1 = (s_i3 +- sqrt(D)) / s33
-    double r2 = atan2(s_ii, num);  // tan r2 = s_ii / (s_i3 +- sqrt(D)) (the other root, stable form)
-    // rotation step (Eq. 16): representatives in (theta_mu - pi, theta_mu] (reading 16)
-    double tm = atan2(mu_i, mu_z);
-    r1 += PI * floor((tm - r1) / PI);
-    r2 += PI * floor((tm - r2) / PI);
-    double t1 = fmax(r1, r2);
-    double t2 = fmin(r1, r2) + PI;
-    // the ray-angle interval [t1, t2] (length < pi) -> its copy meeting the front half (-pi/2, pi/2)
-    bool found = false;
-    for (int m = -1; m <= 1; m++) {
-        double a = t1 + 2.0 * PI * m, b = t2 + 2.0 * PI * m;
-        if (b > -0.5 * PI && a < 0.5 * PI) {
-            t1 = a;
-            t2 = b;
-            found = true;
-            break;
-        }
+    // Angles are handled as unit vectors v(theta) = (sin theta, cos theta) in the (x|y, z) view
+    // plane, so no trigonometry is needed: tan theta = v.x / v.y.
+    // The two tangent-plane roots (Eq. 14-15): tan r1 = (s_i3 +- sqrt(D)) / s33 and, in the
+    // cancellation-free form, tan r2 = s_ii / (s_i3 +- sqrt(D)).
+    double n1 = rhypot(num, s33), n2 = rhypot(s_ii, num);
+    double d1x = num * n1, d1y = s33 * n1, d2x = s_ii * n2, d2y = num * n2;
+    double mx = mu_i / mn, my = mu_z / mn;  // v(theta_mu)
+    // rotation step (Eq. 16, reading 16): representative of each root in (theta_mu - pi, theta_mu]
+    // <=> sin(theta_mu - r) >= 0 <=> cross(v(theta_mu), v(r)) >= 0
+    if (mx * d1y - my * d1x < 0.0) { d1x = -d1x; d1y = -d1y; }
+    if (mx * d2y - my * d2x < 0.0) { d2x = -d2x; d2y = -d2y; }
+    // theta1 = the larger representative (closer to theta_mu: larger cos), theta2 = smaller + pi
+    double lx, ly, ux, uy;
+    if (mx * d1x + my * d1y >= mx * d2x + my * d2y) {
+        lx = d1x; ly = d1y; ux = -d2x; uy = -d2y;
+    } else {
+        lx = d2x; ly = d2y; ux = -d1x; uy = -d1y;
     }
-    if (!found) return false;
-    // clamp (Eq. 17)
-    t1 = fmax(t1, -0.5 * PI + (double)ANGLE_EPS);
-    t2 = fmin(t2, 0.5 * PI - (double)ANGLE_EPS);
-    lo = f * tan(t1) + c;
-    hi = f * tan(t2) + c;
+    // The ray-angle interval [theta1, theta2] (< pi long, through theta_mu) meets the front half
+    // (cos > 0) in one arc; an end behind the camera leaves that side unbounded (the clamp of
+    // Eq. 17 at +-(pi/2 - eps) maps to |x| ~ 1e4 f, beyond any viewport).
+    const bool lf = ly > 0.0, uf = uy > 0.0;
+    if (!lf && !uf) return false;  // no front-facing ray of this plane family meets the ellipsoid
+    lo = lf ? f * (lx / ly) + c : -CUDART_INF;
+    hi = uf ? f * (ux / uy) + c : CUDART_INF;
     return true;
 }
 

@@ -3,7 +3,8 @@
 A pixel passes if the GPU value is within tolerance of the oracle's nominal value, or of
 any admissible variant: flipping the inclusion of contributions whose float64 margin lies in
 the band where float32 can flip it (cutoff |rho^2 - tau| < 4e-3, near plane, Gaussian-level
-inside-test margin) and swapping near-tied neighbours (relative depth gap < 4e-6).
+inside-test margin) and reordering clusters of near-tied contributions (consecutive relative
+depth gaps < 4e-6; FP32 depths carry ~3e-7 relative error, so their order is not determined).
 """
 from __future__ import annotations
 
@@ -14,36 +15,129 @@ import numpy as np
 import oracle as O
 
 CI = {f: i for i, f in enumerate(O.C_FIELDS)}
-MAX_ITEMS = 8
+MAX_VARIANTS = 4096
 
 
 def _variants(c, cfg):
-    """Yield blended (r,g,b,T) for every admissible variant of contribution list c."""
+    """Yield blended (r,g,b,T) for admissible variants of the contribution list c (sorted by z)."""
     n = c.shape[0]
     inc0 = c[:, CI["included"]] > 0.5
     flags = c[:, CI["flags"]].astype(np.int64)
-    toggles = [i for i in range(n) if flags[i] & (O.F_CUTOFF | O.F_NEAR | O.F_GAUSS)]
-    swaps = [i for i in range(n - 1) if (flags[i] & O.F_TIE) and (flags[i + 1] & O.F_TIE)]
-    items = [("t", i) for i in toggles] + [("s", i) for i in swaps]
-    items.sort(key=lambda it: it[1])
-    items = items[:MAX_ITEMS]
-    for mask in itertools.product((0, 1), repeat=len(items)):
+    flippable = (flags & (O.F_CUTOFF | O.F_NEAR | O.F_GAUSS)) != 0
+    seq = [i for i in range(n) if inc0[i] or flippable[i]]
+    z = c[:, CI["z"]]
+    # FP32 depths carry <= ~3e-7 relative error, so only neighbours closer than TIGHT can swap;
+    # the oracle's tie flag (band_tie = 4e-6) marks a superset of those pixels
+    TIGHT = min(cfg["band_tie"], 6e-7)  # 2 x the measured max FP32 z error (2.5e-7)
+    clusters, cur = [], [seq[0]] if seq else []
+    for a, b in zip(seq[:-1], seq[1:]):
+        if (z[b] - z[a]) / max(abs(z[a]), 1e-300) < TIGHT:
+            cur.append(b)
+        else:
+            if len(cur) > 1:
+                clusters.append(cur)
+            cur = [b]
+    if len(cur) > 1:
+        clusters.append(cur)
+    # variant dimensions in depth order, until the product reaches MAX_VARIANTS: inclusion flips,
+    # all orders of small tie clusters, adjacent swaps inside large ones
+    dims = [("t", i) for i in seq if flippable[i]]
+    perms_of = {}
+    for cl in clusters:
+        if len(cl) <= 7:
+            # every order FP32 depths can produce: x may precede y only if z_x - z_y < TIGHT z_y
+            ok = [p for p in itertools.permutations(cl)
+                  if all(z[p[i]] - z[p[j]] < TIGHT * z[p[j]] for i in range(len(p)) for j in range(i + 1, len(p)))]
+            perms_of[tuple(cl)] = ok
+            dims.append(("c", cl))
+        else:
+            for a2, b2 in zip(cl[:-1], cl[1:]):
+                perms_of[(a2, b2)] = [(a2, b2), (b2, a2)]
+                dims.append(("c", [a2, b2]))
+    # rank dimensions by their possible effect on the pixel (alpha x transmittance x colour
+    # contrast along the nominal order) and keep the strongest ones that fit an exhaustive product
+    a = c[:, CI["alpha"]]
+    col = c[:, CI["r"]:CI["b"] + 1]
+    Tn, Tacc = {}, 1.0
+    for i in seq:
+        Tn[i] = Tacc
+        if inc0[i]:
+            Tacc *= 1.0 - a[i]
+
+    def impact(d):
+        if d[0] == "t":
+            i = d[1]
+            return a[i] * Tn[i] * (1.0 + np.abs(col[i]).max())
+        cl = d[1]
+        return Tn[cl[0]] * max(a[x] * a[y] * (1.0 + np.abs(col[x] - col[y]).max()) for x in cl for y in cl if x != y)
+
+    dims.sort(key=impact, reverse=True)
+    n_kept, total = 0, 1
+    for d in dims:  # the strongest prefix that fits an exhaustive product
+        k = 2 if d[0] == "t" else len(perms_of[tuple(d[1])])
+        if total * k > MAX_VARIANTS:
+            break
+        n_kept += 1
+        total *= k
+    choices = []
+    for kind, v in dims:
+        if kind == "t":
+            choices.append([None, v])
+        else:
+            choices.append([(v, p) for p in perms_of[tuple(v)]])
+    # orders are applied in depth order so overlapping pair swaps compose as adjacent transpositions
+    apply_rank = sorted(range(len(dims)), key=lambda k: dims[k][1] if dims[k][0] == "t" else dims[k][1][0])
+
+    def build(combo):
         inc = inc0.copy()
-        order = list(range(n))
-        for on, (kind, i) in zip(mask, items):
-            if not on:
-                continue
+        order = list(seq)
+        for k in apply_rank:
+            ch, (kind, v) = combo[k], dims[k]
             if kind == "t":
-                inc[i] = not inc[i]
+                if ch is not None:
+                    inc[ch] = not inc[ch]
             else:
-                order[i], order[i + 1] = order[i + 1], order[i]
-        yield O.blend_variant(c, inc, np.asarray(order), cfg)
+                cl, perm = ch
+                slots = sorted(order.index(x) for x in cl)
+                for slot, val in zip(slots, perm):
+                    order[slot] = val
+        return O.blend_variant(c, inc, np.asarray(order), cfg)
+
+    target = _variants.target
+    nominal_rest = [ch[0] for ch in choices[n_kept:]]
+    best_e, best_combo = None, None
+    for head in itertools.product(*choices[:n_kept]) if n_kept else [()]:
+        combo = list(head) + nominal_rest
+        v = build(combo)
+        yield v
+        if target is not None:
+            e = np.abs(v[:3] - target[:3]).max()
+            if best_e is None or e < best_e:
+                best_e, best_combo = e, combo
+    if n_kept == len(dims) or target is None:
+        return
+    # the remaining (weaker) ambiguities: coordinate descent from the best exhaustive variant
+    combo = list(best_combo)
+    for _ in range(2):
+        for k in range(len(choices)):
+            bk, bc = None, combo[k]
+            for cand in choices[k]:
+                combo[k] = cand
+                v = build(combo)
+                yield v
+                e = np.abs(v[:3] - target[:3]).max()
+                if bk is None or e < bk:
+                    bk, bc = e, cand
+            combo[k] = bc
+
+
+_variants.target = None
 
 
 def compare(orc: "O.Oracle", gpu: np.ndarray, px, py, tol=5e-4, max_tol=2e-3, frac_req=0.999,
-            max_variant_pixels=400):
-    """gpu: (n, 4) float (r, g, b, T) at pixels (px, py). Returns a report dict; asserts
-    the north-star bar: max |err| <= 2e-3 per channel and >= 99.9% of pixels <= 5e-4."""
+            max_variant_pixels=20000):
+    """gpu: (n, 4) float (r, g, b, T) at pixels (px, py). Returns a report dict; 'ok' is the
+    north-star bar: max |err| <= 2e-3 per channel and >= 99.9% of pixels <= 5e-4."""
     px = np.asarray(px)
     py = np.asarray(py)
     ref, flags, nb = orc.render_pixels(px, py)
@@ -56,16 +150,19 @@ def compare(orc: "O.Oracle", gpu: np.ndarray, px, py, tol=5e-4, max_tol=2e-3, fr
             continue
         c = orc.pixel_contribs(int(px[k]), int(py[k]))
         n_var += 1
+        _variants.target = np.asarray(gpu[k], dtype=np.float64)
         for v in _variants(c, orc.cfg):
             e = np.abs(gpu[k, :3] - v[:3]).max()
             if e < best[k]:
                 best[k] = e
             if best[k] <= tol:
                 break
+    worst = int(np.argmax(best)) if len(best) else 0
     rep = dict(n=len(px), direct_pass=int((err <= tol).sum()), variant_checked=n_var,
                pass_after_variants=int((best <= tol).sum()), max_err=float(best.max()) if len(best) else 0.0,
                max_err_nominal=float(err.max()) if len(err) else 0.0,
                frac_within_tol=float((best <= tol).mean()) if len(best) else 1.0,
-               worst_pixel=(int(px[np.argmax(best)]), int(py[np.argmax(best)])) if len(best) else None)
+               worst_pixel=(int(px[worst]), int(py[worst])) if len(best) else None,
+               worst_flags=int(flags[worst]) if len(best) else 0)
     rep["ok"] = rep["max_err"] <= max_tol and rep["frac_within_tol"] >= frac_req
     return rep
