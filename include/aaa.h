@@ -103,9 +103,9 @@ enum { AAA_FLAG_TIMING = 1u, AAA_FLAG_NO_TILE_CULL = 2u, AAA_FLAG_FORCE_FALLBACK
 /* what for aaa_debug_copy (parity tests only; synchronises) */
 enum {
     AAA_DBG_GAUSS = 0,  /* N x AAA_DBG_GAUSS_FIELDS float64 per-Gaussian preprocess record  */
-    AAA_DBG_KEYS = 1,   /* P uint64 keys, sorted (tile << 32 | depth key)                   */
+    AAA_DBG_KEYS = 1,   /* P uint32 keys, sorted (tile << (32 - tile bits) | log-depth code) */
     AAA_DBG_VALS = 2,   /* P uint32 Gaussian indices, sorted                                  */
-    AAA_DBG_KEYS_UNSORTED = 3, /* P uint64 keys in emission order                         */
+    AAA_DBG_KEYS_UNSORTED = 3, /* P uint32 keys in emission order                         */
     AAA_DBG_VALS_UNSORTED = 4, /* P uint32 values in emission order                       */
     AAA_DBG_RANGES = 5, /* tiles x 2 uint32 [start, end)                                     */
     AAA_DBG_SPILL = 6,   /* spilled pixels: 8 x 32-bit (pixel, list pos, count, T, r, g, b, 0) */

@@ -211,10 +211,15 @@ class Renderer:
 
     def keys_vals(self, sorted_: bool = True):
         if sorted_:
-            return self.debug_copy(AAA_DBG_KEYS, np.uint64), self.debug_copy(AAA_DBG_VALS, np.uint32)
-        k = self.debug_copy(AAA_DBG_KEYS_UNSORTED, np.uint64)
+            return self.debug_copy(AAA_DBG_KEYS, np.uint32), self.debug_copy(AAA_DBG_VALS, np.uint32)
+        k = self.debug_copy(AAA_DBG_KEYS_UNSORTED, np.uint32)
         v = self.debug_copy(AAA_DBG_VALS_UNSORTED, np.uint32)
         return k, v
+
+    def key_tile_shift(self) -> int:
+        """Bits of the depth code in a sort key (key >> this = tile id)."""
+        n_tiles = ((self.width + 15) // 16) * ((self.height + 15) // 16)
+        return min(32 - max(0, (n_tiles - 1).bit_length()), 28)
 
     def ranges(self) -> np.ndarray:
         return self.debug_copy(AAA_DBG_RANGES, np.uint32, 2)

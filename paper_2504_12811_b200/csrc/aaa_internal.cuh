@@ -9,8 +9,11 @@
 namespace aaa {
 
 constexpr int TILE = 16;                // 16x16 pixel tiles (reading 24)
-constexpr int DEPTH_KEY_BITS = 24;      // depth part of the sort key: f32 bits >> 7 (rounds down)
-constexpr int DEPTH_KEY_SHIFT = 7;
+// Sort key (32 bits): tile << key_db | dcode. dcode = floor(S log2(z_lb / near_lo)), a log-depth code
+// over KEY_LOG_RANGE octaves above near (S = 2^key_db / KEY_LOG_RANGE codes per octave); its decode
+// near_lo 2^(dcode / S) is a lower bound of z_lb, so the key stays a valid depth lower bound.
+using skey_t = uint32_t;
+constexpr double KEY_LOG_RANGE = 24.0;
 constexpr int RASTER_REC_F4 = 7;        // raster record: 7 float4 = 112 B
 constexpr float ANGLE_EPS = 1e-4f;      // Eq. 17 epsilon (reading 17)
 constexpr double ZKEY_PAD = 1e-5;       // relative downward pad of the depth key (reading 23)
@@ -34,6 +37,11 @@ struct ViewParams {
     float bg[3];
     uint32_t flags;
     int sh_degree;
+    int key_db;            // depth-code bits of the 32-bit key (32 - tile bits)
+    double key_scale;      // S: codes per octave
+    double key_near;       // near_lo (encode base, = key_near_f promoted)
+    float key_inv_scale_f; // 1/S rounded down (decode)
+    float key_near_f;      // near_lo rounded down (decode)
 };
 
 // Scene residency (L0): structure of float4 arrays, 16-byte aligned.
@@ -48,14 +56,17 @@ struct SceneDev {
     int sh_chunks;
 };
 
-// K3 input per visible Gaussian (80 B): screen-space quadratic q(p) = N(p) - tau Q(p) relative
-// to p_ref (exact tile predicate for non-crossing Gaussians, K3), tile rect, key.
+// K3 input per visible Gaussian (112 B): screen-space quadratic q(p) = N(p) - tau Q(p) relative
+// to p_ref (exact tile predicate for non-crossing Gaussians, K3) with its per-Gaussian
+// box-minimum helpers precomputed (no FP64 division per tile), tile rect, key.
 struct __align__(16) CullRec {
     double qa, qb, qc, qd, qe, qf;  // q = qa dx^2 + 2 qb dx dy + qc dy^2 + 2 qd dx + 2 qe dy + qf
+    double ia, ic;                  // 1/qa, 1/qc when positive (edge critical points), else 0
+    double xs, ys, qi;              // interior critical point and its value (qi = +inf unless PD)
     float pref_x, pref_y;
     uint16_t tx0, ty0, tx1, ty1;    // inclusive tile rect (band-clipped)
     int32_t cross_slot;             // >= 0: index into CrossRec (exact QP path); -1 otherwise
-    uint32_t zkey;                  // depth key (24 bits)
+    uint32_t zkey;                  // depth code (key_db bits)
 };
 
 // Gaussians whose tau-ellipsoid reaches z <= near: the exact QP fallback needs T_view.
@@ -94,10 +105,10 @@ void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, b
 size_t scan_state_words(int64_t n);
 void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, uint32_t* state, uint32_t* ticket,
                  cudaStream_t st);
-void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, uint64_t* keys,
+void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, skey_t* keys,
                       uint32_t* vals, uint32_t* state, cudaStream_t st);
 struct SortBufs {
-    uint64_t* keys[2];
+    skey_t* keys[2];
     uint32_t* vals[2];
     uint32_t* hist;        // passes * 256
     uint32_t* state;       // passes * blocks * 256
@@ -108,7 +119,7 @@ int sort_passes(int key_bits);
 size_t sort_state_words(uint32_t cap, int passes);
 // returns the index (0/1) of the buffer holding the sorted output
 int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st);
-void launch_ranges(const uint64_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles,
+void launch_ranges(const skey_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles, int key_db,
                    cudaStream_t st);
 // exact state of a pixel whose K6 window filled: K6s resumes it at list position `pos`
 struct SpillHdr {
@@ -117,7 +128,7 @@ struct SpillHdr {
     uint32_t pad;
 };
 struct RasterArgs {
-    const uint64_t* keys;
+    const skey_t* keys;
     const uint32_t* vals;
     const uint2* ranges;
     const float4* raster;

@@ -134,6 +134,18 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     for (int i = 0; i < 3; i++) vp.bg[i] = ctx->cfg.background[i];
     vp.flags = ctx->cfg.flags;
     vp.sh_degree = ctx->scene.sh_degree;
+    // 32-bit sort key: tile bits + log-depth code bits (see aaa_internal.cuh)
+    int tb = 0;
+    while ((1u << tb) < (uint32_t)(vp.tiles_x * vp.tiles_y)) tb++;
+    vp.key_db = std::min(32 - tb, 28);
+    vp.key_scale = std::ldexp(1.0, vp.key_db) / KEY_LOG_RANGE;
+    float nl = (float)(c.near_z * (1.0 - 1e-5));
+    if ((double)nl > c.near_z * (1.0 - 1e-5)) nl = std::nextafter(nl, 0.f);
+    vp.key_near_f = nl;
+    vp.key_near = (double)nl;
+    float is = (float)(1.0 / vp.key_scale);
+    if ((double)is > 1.0 / vp.key_scale) is = std::nextafter(is, 0.f);
+    vp.key_inv_scale_f = is;
     return vp;
 }
 
@@ -201,7 +213,7 @@ aaa_status ensure_pairs(aaa_ctx* ctx, uint32_t C, int passes) {
         }
         uint32_t cap = C + C / 4 + 4096;
         for (int i = 0; i < 2; i++) {
-            CU(cudaMalloc(&ctx->sb.keys[i], (size_t)cap * sizeof(uint64_t)));
+            CU(cudaMalloc(&ctx->sb.keys[i], (size_t)cap * sizeof(skey_t)));
             CU(cudaMalloc(&ctx->sb.vals[i], (size_t)cap * sizeof(uint32_t)));
         }
         ctx->pair_cap = cap;
@@ -257,7 +269,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     CU(cudaMemcpyAsync(ctx->h_counters, ctx->vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     const uint32_t C = ctx->h_counters[CNT_C];
-    const int key_bits = DEPTH_KEY_BITS + bits_for((uint32_t)(vp.tiles_x * vp.tiles_y));
+    const int key_bits = 32;
     s = ensure_pairs(ctx, C, sort_passes(key_bits));
     if (s) return s;
     mark(3);
@@ -277,7 +289,8 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     int sorted = launch_sort(ctx->sb, &ctx->vb.counters[CNT_P], C, key_bits, st);
     ctx->last_sorted = sorted;
     mark(5);
-    launch_ranges(ctx->sb.keys[sorted], &ctx->vb.counters[CNT_P], C, ctx->ranges, vp.tiles_x * vp.tiles_y, st);
+    launch_ranges(ctx->sb.keys[sorted], &ctx->vb.counters[CNT_P], C, ctx->ranges, vp.tiles_x * vp.tiles_y, vp.key_db,
+                  st);
     mark(6);
     if (C > 0) ctx->launches += 3 + sort_passes(key_bits);
     RasterArgs ra{};
@@ -526,11 +539,11 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
     uint32_t P = 0;
     CU(cudaMemcpyAsync(&P, &ctx->vb.counters[CNT_P], sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    std::vector<uint64_t> keys(P);
-    if (P) CU(cudaMemcpy(keys.data(), ctx->sb.keys[0], P * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    std::vector<skey_t> keys(P);
+    if (P) CU(cudaMemcpy(keys.data(), ctx->sb.keys[0], P * sizeof(skey_t), cudaMemcpyDeviceToHost));
     const int tx = (ctx->cam.width + TILE - 1) / TILE;
     for (int r = 0; r < n_rows; r++) out[r] = 0;
-    for (uint32_t i = 0; i < P; i++) out[(keys[i] >> DEPTH_KEY_BITS) / tx]++;
+    for (uint32_t i = 0; i < P; i++) out[(keys[i] >> ctx->last_vp.key_db) / tx]++;
     return AAA_OK;
 }
 
@@ -604,7 +617,7 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
     CU(cudaStreamSynchronize(ctx->stream));
     uint32_t h[CNT_TOTAL];
     CU(cudaMemcpy(h, ctx->vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
-    if (what == AAA_DBG_KEYS || what == AAA_DBG_KEYS_UNSORTED) bytes = (size_t)h[CNT_P] * 8;
+    if (what == AAA_DBG_KEYS || what == AAA_DBG_KEYS_UNSORTED) bytes = (size_t)h[CNT_P] * sizeof(skey_t);
     if (what == AAA_DBG_VALS || what == AAA_DBG_VALS_UNSORTED) bytes = (size_t)h[CNT_P] * 4;
     if (what == AAA_DBG_RANGES) bytes = (size_t)ctx->last_vp.tiles_x * ctx->last_vp.tiles_y * sizeof(uint2);
     if (what == AAA_DBG_SPILL) bytes = (size_t)std::min((size_t)h[CNT_SPILL], ctx->spill_cap) * sizeof(SpillHdr);

@@ -16,43 +16,55 @@
 
 namespace aaa {
 
-constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS;
+constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS, EMIT_SOFF = 4096;
 
 __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const CullRec* __restrict__ cull,
                                                             const CrossRec* __restrict__ cross,
                                                             const uint32_t* __restrict__ offsets, int64_t n,
-                                                            uint32_t C, uint64_t* __restrict__ keys,
+                                                            uint32_t C, skey_t* __restrict__ keys,
                                                             uint32_t* __restrict__ vals, uint32_t* counters,
                                                             uint32_t* state) {
     __shared__ uint32_t s_scan[32];
     __shared__ uint32_t s_ticket, s_excl;
-    __shared__ int64_t s_g0;
+    __shared__ int64_t s_g0, s_g1;
+    __shared__ uint32_t s_off[EMIT_SOFF];
     if (threadIdx.x == 0) {
         uint32_t t = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
         s_ticket = t;
-        // last Gaussian whose offset <= first candidate of the chunk
-        uint32_t c0 = t * EMIT_CHUNK;
-        int64_t lo = 0, hi = n;  // find largest g with offsets[g] <= c0
+        // the chunk's candidates [c0, c1] belong to Gaussians [g0, g1]: largest g with offset <= c
+        uint32_t c0 = t * EMIT_CHUNK, c1 = min(c0 + EMIT_CHUNK, C) - 1;
+        int64_t lo = 0, hi = n;
         while (hi - lo > 1) {
             int64_t mid = (lo + hi) >> 1;
             if (offsets[mid] <= c0) lo = mid; else hi = mid;
         }
         s_g0 = lo;
-    }
-    __syncthreads();
-    uint32_t chunk = s_ticket;
-    uint32_t cbeg = chunk * EMIT_CHUNK + threadIdx.x * EMIT_ITEMS;
-    // this thread's first Gaussian: advance from the chunk's first Gaussian
-    int64_t g = s_g0;
-    {
-        int64_t lo = g, hi = n;
+        hi = n;
         while (hi - lo > 1) {
             int64_t mid = (lo + hi) >> 1;
-            if (offsets[mid] <= cbeg) lo = mid; else hi = mid;
+            if (offsets[mid] <= c1) lo = mid; else hi = mid;
         }
-        g = lo;
+        s_g1 = lo;
     }
-    uint64_t key[EMIT_ITEMS];
+    __syncthreads();
+    const uint32_t chunk = s_ticket;
+    const uint32_t cbeg = chunk * EMIT_CHUNK + threadIdx.x * EMIT_ITEMS;
+    const int64_t g0 = s_g0, g1 = s_g1;
+    const bool in_smem = g1 - g0 + 1 <= EMIT_SOFF;  // offsets of the chunk's Gaussians staged in smem
+    if (in_smem)
+        for (int64_t i = threadIdx.x; i <= g1 - g0; i += EMIT_THREADS) s_off[i] = offsets[g0 + i];
+    __syncthreads();
+    auto off = [&](int64_t x) -> uint32_t { return in_smem ? s_off[x - g0] : offsets[x]; };
+    auto find = [&](uint32_t c, int64_t lo) -> int64_t {  // largest g in [lo, g1] with off(g) <= c
+        int64_t hi = g1 + 1;
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (off(mid) <= c) lo = mid; else hi = mid;
+        }
+        return lo;
+    };
+    int64_t g = find(cbeg, g0);
+    skey_t key[EMIT_ITEMS];
     uint32_t val[EMIT_ITEMS];
     uint32_t keep_mask = 0, nkeep = 0;
     const bool no_cull = (vp.flags & AAA_FLAG_NO_TILE_CULL) != 0;
@@ -60,16 +72,9 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
     for (int k = 0; k < EMIT_ITEMS; k++) {
         uint32_t c = cbeg + k;
         if (c >= C) break;
-        if (g + 1 < n && offsets[g + 1] <= c) {  // next Gaussian with candidates (skip empty runs)
-            int64_t lo = g + 1, hi = n;
-            while (hi - lo > 1) {
-                int64_t mid = (lo + hi) >> 1;
-                if (offsets[mid] <= c) lo = mid; else hi = mid;
-            }
-            g = lo;
-        }
+        if (g < g1 && off(g + 1) <= c) g = find(c, g + 1);  // next Gaussian (skips empty runs)
         const CullRec& r = cull[g];
-        uint32_t j = c - offsets[g];
+        uint32_t j = c - off(g);
         uint32_t w = (uint32_t)r.tx1 - r.tx0 + 1;
         int tx = r.tx0 + (int)(j % w), ty = r.ty0 + (int)(j / w);
         double x0 = TILE * tx + 0.5, x1 = fmin(TILE * tx + TILE - 0.5, vp.width - 0.5);
@@ -80,7 +85,8 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
             keep = true;
         } else if (r.cross_slot < 0) {
             double px = r.pref_x, py = r.pref_y;
-            keep = quad_box_min(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, x0 - px, x1 - px, y0 - py, y1 - py) < 0.0;
+            keep = quad_box_min_pre(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, r.ia, r.ic, r.xs, r.ys, r.qi, x0 - px,
+                                    x1 - px, y0 - py, y1 - py) < 0.0;
             if (keep) {
                 // the same exact test on each 8x4 warp sub-tile (pixel-centre rects): the raster
                 // kernels skip the Gaussian on sub-tiles whose bit is clear ("repeated culling")
@@ -90,7 +96,8 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
                     double sx0 = TILE * tx + 8 * (s & 1) + 0.5, sy0 = TILE * ty + 4 * (s >> 1) + 0.5;
                     if (sx0 > vp.width - 0.5 || sy0 > vp.height - 0.5) continue;
                     double sx1 = fmin(sx0 + 7.0, vp.width - 0.5), sy1 = fmin(sy0 + 3.0, vp.height - 0.5);
-                    if (quad_box_min(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, sx0 - px, sx1 - px, sy0 - py, sy1 - py) < 0.0)
+                    if (quad_box_min_pre(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, r.ia, r.ic, r.xs, r.ys, r.qi,
+                                         sx0 - px, sx1 - px, sy0 - py, sy1 - py) < 0.0)
                         sub |= 1u << s;
                 }
             }
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
         }
         if (keep) {
             uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
-            key[k] = ((uint64_t)tile << DEPTH_KEY_BITS) | r.zkey;
+            key[k] = (tile << vp.key_db) | r.zkey;
             val[k] = (uint32_t)g | (sub << VAL_INDEX_BITS);
             keep_mask |= 1u << k;
             nkeep++;
@@ -125,7 +132,7 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
     if (threadIdx.x == 0 && (uint64_t)(chunk + 1) * EMIT_CHUNK >= C) counters[CNT_P] = s_excl + btot;
 }
 
-void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, uint64_t* keys,
+void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, skey_t* keys,
                       uint32_t* vals, uint32_t* state, cudaStream_t st) {
     if (C == 0) return;
     unsigned blocks = (C + EMIT_CHUNK - 1) / EMIT_CHUNK;

@@ -56,6 +56,27 @@ __device__ __forceinline__ double quad_box_min(double a, double b, double c, dou
     return m;
 }
 
+// quad_box_min with the per-Gaussian parts precomputed: ia = 1/a (a > 0) else 0, ic likewise,
+// (xs, ys, qi) the interior critical point and value (qi = +inf unless q is positive definite).
+__device__ __forceinline__ double quad_box_min_pre(double a, double b, double c, double d, double e, double f,
+                                                   double ia, double ic, double xs, double ys, double qi,
+                                                   double x0, double x1, double y0, double y1) {
+    auto q = [&](double x, double y) { return (a * x + 2.0 * b * y + 2.0 * d) * x + (c * y + 2.0 * e) * y + f; };
+    double m = fmin(fmin(q(x0, y0), q(x1, y0)), fmin(q(x0, y1), q(x1, y1)));
+    if (ic > 0.0) {
+        double ya = -(b * x0 + e) * ic, yb = -(b * x1 + e) * ic;
+        if (ya > y0 && ya < y1) m = fmin(m, q(x0, ya));
+        if (yb > y0 && yb < y1) m = fmin(m, q(x1, yb));
+    }
+    if (ia > 0.0) {
+        double xa = -(b * y0 + d) * ia, xb = -(b * y1 + d) * ia;
+        if (xa > x0 && xa < x1) m = fmin(m, q(xa, y0));
+        if (xb > x0 && xb < x1) m = fmin(m, q(xb, y1));
+    }
+    if (xs >= x0 && xs <= x1 && ys >= y0 && ys <= y1) m = fmin(m, qi);
+    return m;
+}
+
 // Exact minimum of rho^2 = |u|^2 over the frustum {pixel-centre rect [x0,x1]x[y0,y1]} ∩
 // {z >= near} (readings 20-21). The five view-space half-spaces n.x + d >= 0 are
 // pulled back to Gaussian space through x = M u + mu_v (Eq. 5); the convex QP is solved by

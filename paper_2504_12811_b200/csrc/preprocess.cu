@@ -315,8 +315,10 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, ViewParams vp, 
     double gp[3] = {gz[0] - gc * ch[0], gz[1] - gc * ch[1], gz[2] - gc * ch[2]};
     double zlb = muv[2] - sqrt(tau) * sqrt(dot3(gp, gp)) - (tau / cn) * fmax(0.0, -gc);
     zlb = fmax(zlb, vp.near_z);
-    float zf = __double2float_rd(zlb * (1.0 - ZKEY_PAD));
-    uint32_t zkey = __float_as_uint(zf) >> DEPTH_KEY_SHIFT;
+    // log-depth code, rounded down (decode <= z_lb (1 - pad)); zlb >= near > near_lo keeps u >= 0
+    const double u = vp.key_scale * log2(zlb * (1.0 - ZKEY_PAD) / vp.key_near);
+    const double qmax = (double)((1u << vp.key_db) - 1u);
+    uint32_t zkey = (uint32_t)fmin(fmax(floor(u), 0.0), qmax);
 
     // --- colour (reading 15): SH at d = (mu - o)/|mu - o|
     float rgb[3];
@@ -334,6 +336,19 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, ViewParams vp, 
     }
     CullRec cu;
     cu.qa = qa; cu.qb = qb; cu.qc = qc; cu.qd = qd; cu.qe = qe; cu.qf = qf;
+    cu.ia = qa > 0.0 ? 1.0 / qa : 0.0;
+    cu.ic = qc > 0.0 ? 1.0 / qc : 0.0;
+    {
+        double det = qa * qc - qb * qb;
+        if (qa > 0.0 && det > 0.0) {
+            cu.xs = (qb * qe - qc * qd) / det;
+            cu.ys = (qb * qd - qa * qe) / det;
+            cu.qi = (qa * cu.xs + 2.0 * qb * cu.ys + 2.0 * qd) * cu.xs + (qc * cu.ys + 2.0 * qe) * cu.ys + qf;
+        } else {
+            cu.xs = cu.ys = 0.0;
+            cu.qi = CUDART_INF;
+        }
+    }
     cu.pref_x = prx_f;
     cu.pref_y = pry_f;
     cu.tx0 = (uint16_t)tx0; cu.ty0 = (uint16_t)ty0; cu.tx1 = (uint16_t)tx1; cu.ty1 = (uint16_t)ty1;
@@ -358,7 +373,7 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, ViewParams vp, 
         dbg[11] = rgb[0]; dbg[12] = rgb[1]; dbg[13] = rgb[2];
         dbg[14] = 1.0;
         dbg[16] = tx0; dbg[17] = ty0; dbg[18] = tx1; dbg[19] = ty1;
-        dbg[20] = (double)__uint_as_float(zkey << DEPTH_KEY_SHIFT);
+        dbg[20] = vp.key_near * exp2((double)zkey / vp.key_scale);
         dbg[25] = zlb;
     }
 }

@@ -9,8 +9,7 @@
 //    (match.any + popc, stable within the warp), publishes its per-digit counts with a
 //    decoupled look-back over CTAs taken in ticket order, reorders the keys in shared memory
 //    and writes digit runs (reads 12 B, writes 12 B per key per pass).
-// Key layout: tile << 24 | depth24 (depth24 = f32 bits >> 7 of a positive lower bound, so
-// truncation rounds down and keeps the bound valid). Key bits = 24 + tile bits; 8-bit digits.
+// Keys are 32-bit (tile << key_db | log-depth code, see aaa_internal.cuh): 4 passes of 8-bit digits.
 #include "aaa_internal.cuh"
 #include "lookback.cuh"
 
@@ -26,14 +25,14 @@ size_t sort_state_words(uint32_t cap, int passes) {
     return (size_t)passes * blocks * 256;
 }
 
-__global__ void __launch_bounds__(256) k_sort_hist(const uint64_t* __restrict__ keys, const uint32_t* d_count,
+__global__ void __launch_bounds__(256) k_sort_hist(const skey_t* __restrict__ keys, const uint32_t* d_count,
                                                     int passes, uint32_t* hist) {
     __shared__ uint32_t sh[MAX_PASSES * 256];
     for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     uint32_t P = *d_count;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-        uint64_t k = keys[i];
+        skey_t k = keys[i];
         for (int p = 0; p < passes; p++) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 0xFF)], 1u);
     }
     __syncthreads();
@@ -50,14 +49,14 @@ __global__ void k_sort_hist_scan(uint32_t* hist) {
     h[threadIdx.x] = e;
 }
 
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __restrict__ kin,
+__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const skey_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin,
-                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                           skey_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            const uint32_t* d_count, int shift,
                                                            const uint32_t* __restrict__ digit_base,
                                                            uint32_t* state, uint32_t* ticket_ctr) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);                       // SORT_TILE
+    skey_t* s_keys = reinterpret_cast<skey_t*>(smem);                             // SORT_TILE
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + SORT_TILE);          // SORT_TILE
     uint32_t* s_whist = s_vals + SORT_TILE;                                      // SORT_WARPS * 256
     uint32_t* s_base = s_whist + SORT_WARPS * 256;                               // 256 (global base per digit)
@@ -75,7 +74,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
 
-    uint64_t k[SORT_ITEMS];
+    skey_t k[SORT_ITEMS];
     uint32_t v[SORT_ITEMS];
     uint32_t rank[SORT_ITEMS];
     // warp w owns the contiguous segment [w*512, w*512+512) of the tile, round r covers 32 keys
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
     for (int r = 0; r < SORT_ITEMS; r++) {
         uint64_t idx = start + w * (SORT_ITEMS * 32) + r * 32 + lane;
         bool valid = idx < P;
-        k[r] = valid ? kin[idx] : ~0ull;
+        k[r] = valid ? kin[idx] : ~0u;
         v[r] = valid ? vin[idx] : 0u;
     }
 #pragma unroll
@@ -148,7 +147,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
     __syncthreads();
     uint32_t nvalid = (uint32_t)min((uint64_t)SORT_TILE, (uint64_t)P - start);
     for (uint32_t i = threadIdx.x; i < nvalid; i += SORT_THREADS) {
-        uint64_t key = s_keys[i];
+        skey_t key = s_keys[i];
         uint32_t d = (uint32_t)((key >> shift) & 0xFF);
         uint32_t o = s_base[d] + i;
         kout[o] = key;
@@ -157,7 +156,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
 }
 
 static size_t onesweep_smem() {
-    return (size_t)SORT_TILE * 12 + (SORT_WARPS * 256 + 256 + 256 + 32 + 4) * 4;
+    return (size_t)SORT_TILE * (sizeof(skey_t) + 4) + (SORT_WARPS * 256 + 256 + 256 + 32 + 4) * 4;
 }
 
 int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st) {
@@ -188,21 +187,21 @@ int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bit
 }
 
 // ------------------------------------------------------------------ K5: tile ranges
-__global__ void k_ranges(const uint64_t* __restrict__ keys, const uint32_t* d_count, uint2* ranges) {
+__global__ void k_ranges(const skey_t* __restrict__ keys, const uint32_t* d_count, uint2* ranges, int key_db) {
     uint32_t P = *d_count;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-        uint32_t t = (uint32_t)(keys[i] >> DEPTH_KEY_BITS);
-        if (i == 0 || (uint32_t)(keys[i - 1] >> DEPTH_KEY_BITS) != t) ranges[t].x = i;
-        if (i + 1 == P || (uint32_t)(keys[i + 1] >> DEPTH_KEY_BITS) != t) ranges[t].y = i + 1;
+        uint32_t t = keys[i] >> key_db;
+        if (i == 0 || (keys[i - 1] >> key_db) != t) ranges[t].x = i;
+        if (i + 1 == P || (keys[i + 1] >> key_db) != t) ranges[t].y = i + 1;
     }
 }
 
-void launch_ranges(const uint64_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles,
+void launch_ranges(const skey_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles, int key_db,
                    cudaStream_t st) {
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * n_tiles, st);
     if (cap == 0) return;
     unsigned blocks = min((cap + 255) / 256, 148u * 8u);
-    k_ranges<<<blocks, 256, 0, st>>>(keys, d_count, ranges);
+    k_ranges<<<blocks, 256, 0, st>>>(keys, d_count, ranges, key_db);
 }
 
 }  // namespace aaa

