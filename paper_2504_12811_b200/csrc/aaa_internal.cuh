@@ -56,7 +56,7 @@ struct SceneDev {
     int sh_chunks;
 };
 
-// K3 input per visible Gaussian (112 B): screen-space quadratic q(p) = N(p) - tau Q(p) relative
+// K3 input per visible Gaussian (128 B): screen-space quadratic q(p) = N(p) - tau Q(p) relative
 // to p_ref (exact tile predicate for non-crossing Gaussians, K3) with its per-Gaussian
 // box-minimum helpers precomputed (no FP64 division per tile), tile rect, key.
 struct __align__(16) CullRec {
@@ -65,11 +65,12 @@ struct __align__(16) CullRec {
     double xs, ys, qi;              // interior critical point and its value (qi = +inf unless PD)
     float pref_x, pref_y;
     uint16_t tx0, ty0, tx1, ty1;    // inclusive tile rect (band-clipped)
+    uint16_t i0, j0, i1, j1;        // inclusive pixel rect of the bounds (sub-tile pre-reject)
     int32_t cross_slot;             // >= 0: index into CrossRec (exact QP path); -1 otherwise
-    uint32_t zkey;                  // depth code (key_db bits)
+    uint32_t zkey;                  // log-depth code of the depth lower bound (reading 23)
 };
 
-// Gaussians whose tau-ellipsoid reaches z <= near: the exact QP fallback needs T_view.
+// Gaussians whose tau-ellipsoid reaches z <= near: the exact QP culling path needs T_view.
 struct CrossRec {
     double M[9];    // view <- Gaussian-space linear map (row-major), filtered scales
     double muv[3];

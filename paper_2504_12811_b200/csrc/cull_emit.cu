@@ -93,7 +93,10 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
                 sub = 0;
 #pragma unroll
                 for (int s = 0; s < 8; s++) {
-                    double sx0 = TILE * tx + 8 * (s & 1) + 0.5, sy0 = TILE * ty + 4 * (s >> 1) + 0.5;
+                    const int spx = TILE * tx + 8 * (s & 1), spy = TILE * ty + 4 * (s >> 1);
+                    // sub-tiles outside the Gaussian's pixel rect hold no contributing pixel (bounds)
+                    if (spx > r.i1 || spx + 7 < r.i0 || spy > r.j1 || spy + 3 < r.j0) continue;
+                    double sx0 = spx + 0.5, sy0 = spy + 0.5;
                     if (sx0 > vp.width - 0.5 || sy0 > vp.height - 0.5) continue;
                     double sx1 = fmin(sx0 + 7.0, vp.width - 0.5), sy1 = fmin(sy0 + 3.0, vp.height - 0.5);
                     if (quad_box_min_pre(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, r.ia, r.ic, r.xs, r.ys, r.qi,

@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, ViewParams vp, 
     cu.pref_x = prx_f;
     cu.pref_y = pry_f;
     cu.tx0 = (uint16_t)tx0; cu.ty0 = (uint16_t)ty0; cu.tx1 = (uint16_t)tx1; cu.ty1 = (uint16_t)ty1;
+    cu.i0 = (uint16_t)i0; cu.j0 = (uint16_t)j0; cu.i1 = (uint16_t)i1; cu.j1 = (uint16_t)j1;
     cu.cross_slot = slot;
     cu.zkey = zkey;
     vb.cull[g] = cu;
