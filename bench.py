@@ -241,7 +241,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.empty_cache()
     H, W = views[0].height, views[0].width
     out = torch.empty((len(views), 3, H, W), dtype=torch.float32, device=dev)
-    R.set_config(flags=pkg.AAA_FLAG_TIMING)
+    R.set_config(flags=pkg.AAA_FLAG_TIMING, window_k=int(os.environ.get("AAA_WINDOW_K", "32")))
 
     def step():
         R.render_batch(views, out_rgb=out)

@@ -562,6 +562,10 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     out->unresolved_pixels = h[CNT_UNRESOLVED];
     out->crossing = h[CNT_CROSS];
     out->evaluations = h[CNT_EVAL];
+#ifdef AAA_DEBUG_STATS
+    fprintf(stderr, "[aaa debug] shifts=%llu inserts=%llu\n", *(unsigned long long*)&h[20],
+            *(unsigned long long*)&h[22]);
+#endif
     out->launches = ctx->launches;
     // per-stage means over the timed views since the previous call
     // stages: K1, K2, K3, sort, ranges, K6, K6b+K6c, host-sync gap, output copy, total
