@@ -1,8 +1,13 @@
 // api.cu — the C ABI (include/aaa.h): context, scene residency, per-view pipeline driver.
 //
-// Pipeline per view (all on the context's stream):
-//   K1 preprocess -> K2 scan -> [one 16-byte D2H of the counters, the only host sync] ->
-//   K3 cull+emit -> K4 onesweep sort -> K5 ranges -> K6 raster (+ K6b / K6c fallbacks).
+// Pipeline per view:
+//   prep stream:   K1 preprocess -> K2 scan -> [one 16-byte D2H of the counters, the only host
+//                  sync] -> K3 cull+emit -> K4 onesweep sort -> K5 ranges
+//   raster stream: K6 raster -> K6s spill resolution -> (host outputs) D2H image copy
+// Every per-view buffer lives in one of two slots used alternately, so view v+1's K1-K5 run on
+// the (high-priority) prep stream while view v's K6/K6s still occupy the (low-priority) raster
+// stream; the events prep_done / raster_done of a slot order the two streams. Both streams are
+// library-owned and non-blocking; the caller's stream is joined at entry and exit of each call.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -15,13 +20,10 @@
 
 using namespace aaa;
 
-struct aaa_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    aaa_config cfg{};
-    aaa_camera cam{};
-    bool have_cam = false, loaded = false;
-    SceneDev scene{};
+namespace {
+
+// all buffers one view in flight needs (the scene is shared by both slots)
+struct Slot {
     ViewBufs vb{};
     int64_t vb_n = -1;
     size_t scan_state_cap = 0;
@@ -34,22 +36,38 @@ struct aaa_ctx {
     float4* spill_e = nullptr;
     size_t spill_cap = 0;
     int spill_k = 0;
-    uint32_t* h_counters = nullptr;  // pinned
-    float* d_out = nullptr;
+    float* d_out = nullptr;  // staging image for host outputs
     size_t d_out_cap = 0;
+    cudaEvent_t prep_done = nullptr, raster_done = nullptr;
+    ViewParams vp{};
+    uint32_t C = 0;
+    int sorted = 0;
+};
+
+}  // namespace
+
+struct aaa_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;             // caller's stream
+    cudaStream_t pstream = nullptr, rstream = nullptr;  // prep (high priority) / raster (low priority)
+    cudaEvent_t ev_entry = nullptr, ev_exit = nullptr;
+    aaa_config cfg{};
+    aaa_camera cam{};
+    bool have_cam = false, loaded = false;
+    SceneDev scene{};
+    Slot slot[2];
+    int cur = 0;  // slot of the last view
+    uint32_t* h_counters = nullptr;  // pinned
     std::string err;
-    // last view bookkeeping
-    ViewParams last_vp{};
-    uint32_t last_C = 0;
-    int last_sorted = 0;
-    int last_key_bits = 0;
     // per-view stage events (AAA_FLAG_TIMING): a pool reused across views, read at get_stats
     std::vector<std::vector<cudaEvent_t>> ev_pool;
     size_t ev_used = 0;
     int64_t launches = 0;
 };
 
-constexpr int N_EV = 10;  // e0 K1 e1 K2 e2 [sync] e3 K3 e4 sort e5 ranges e6 K6 e7 K6b/c e8 [copy] e9
+// prep stream:   e0 K1 e1 K2 e2 [sync] e3 K3 e4 sort e5 ranges e6
+// raster stream: e10 K6 e7 K6s e8 [copy] e9
+constexpr int N_EV = 11;
 
 namespace {
 
@@ -149,15 +167,21 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     return vp;
 }
 
-int bits_for(uint32_t v) {  // bits to represent values < v
-    int b = 0;
-    while ((1ull << b) < v) b++;
-    return b;
+void free_slot(Slot& s) {
+    ViewBufs& vb = s.vb;
+    cudaFree(vb.cull); cudaFree(vb.raster); cudaFree(vb.color); cudaFree(vb.counts); cudaFree(vb.offsets);
+    cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
+    for (int i = 0; i < 2; i++) { cudaFree(s.sb.keys[i]); cudaFree(s.sb.vals[i]); }
+    cudaFree(s.sb.hist); cudaFree(s.sb.state); cudaFree(s.sb.tickets);
+    cudaFree(s.ranges); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.d_out);
+    if (s.prep_done) cudaEventDestroy(s.prep_done);
+    if (s.raster_done) cudaEventDestroy(s.raster_done);
+    s = Slot{};
 }
 
-aaa_status ensure_view_bufs(aaa_ctx* ctx, int64_t n) {
-    if (ctx->vb_n >= n && ctx->vb.counters) return AAA_OK;
-    ViewBufs& vb = ctx->vb;
+aaa_status ensure_view_bufs(aaa_ctx* ctx, Slot& sl, int64_t n) {
+    if (sl.vb_n >= n && sl.vb.counters) return AAA_OK;
+    ViewBufs& vb = sl.vb;
     cudaFree(vb.cull); cudaFree(vb.raster); cudaFree(vb.color); cudaFree(vb.counts); cudaFree(vb.offsets);
     cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters);
     uint32_t* keep_state = vb.scan_state;
@@ -171,16 +195,17 @@ aaa_status ensure_view_bufs(aaa_ctx* ctx, int64_t n) {
     CU(cudaMalloc(&vb.offsets, m * sizeof(uint32_t)));
     CU(cudaMalloc(&vb.cross, m * sizeof(CrossRec)));
     CU(cudaMalloc(&vb.counters, CNT_TOTAL * sizeof(uint32_t)));
-    ctx->vb_n = n;
+    CU(cudaMemset(vb.counters, 0, CNT_TOTAL * sizeof(uint32_t)));
+    sl.vb_n = n;
     return AAA_OK;
 }
 
-aaa_status ensure_tiles(aaa_ctx* ctx, int n_tiles) {
-    if (n_tiles <= ctx->ranges_cap) return AAA_OK;
-    cudaFree(ctx->ranges);
-    ctx->ranges = nullptr;
-    CU(cudaMalloc(&ctx->ranges, (size_t)n_tiles * sizeof(uint2)));
-    ctx->ranges_cap = n_tiles;
+aaa_status ensure_tiles(aaa_ctx* ctx, Slot& sl, int n_tiles) {
+    if (n_tiles <= sl.ranges_cap) return AAA_OK;
+    cudaFree(sl.ranges);
+    sl.ranges = nullptr;
+    CU(cudaMalloc(&sl.ranges, (size_t)n_tiles * sizeof(uint2)));
+    sl.ranges_cap = n_tiles;
     return AAA_OK;
 }
 
@@ -188,60 +213,69 @@ aaa_status ensure_tiles(aaa_ctx* ctx, int n_tiles) {
 // pixel is counted as unresolved by aaa_get_stats), each holding the window's K entries.
 constexpr size_t MAX_SPILL = (size_t)1 << 22;
 
-aaa_status ensure_spill(aaa_ctx* ctx, size_t pixels, int k) {
+aaa_status ensure_spill(aaa_ctx* ctx, Slot& sl, size_t pixels, int k) {
     size_t cap = std::min(pixels, MAX_SPILL);
-    if (cap <= ctx->spill_cap && k <= ctx->spill_k) return AAA_OK;
-    cudaFree(ctx->spill_hdr);
-    cudaFree(ctx->spill_e);
-    ctx->spill_hdr = nullptr;
-    ctx->spill_e = nullptr;
-    ctx->spill_cap = 0;
-    CU(cudaMalloc(&ctx->spill_hdr, cap * sizeof(SpillHdr)));
-    CU(cudaMalloc(&ctx->spill_e, cap * (size_t)k * sizeof(float4)));
-    ctx->spill_cap = cap;
-    ctx->spill_k = k;
+    if (cap <= sl.spill_cap && k <= sl.spill_k) return AAA_OK;
+    cudaFree(sl.spill_hdr);
+    cudaFree(sl.spill_e);
+    sl.spill_hdr = nullptr;
+    sl.spill_e = nullptr;
+    sl.spill_cap = 0;
+    CU(cudaMalloc(&sl.spill_hdr, cap * sizeof(SpillHdr)));
+    CU(cudaMalloc(&sl.spill_e, cap * (size_t)k * sizeof(float4)));
+    sl.spill_cap = cap;
+    sl.spill_k = k;
     return AAA_OK;
 }
 
-aaa_status ensure_pairs(aaa_ctx* ctx, uint32_t C, int passes) {
-    if (C > ctx->pair_cap || !ctx->sb.keys[0]) {
+aaa_status ensure_pairs(aaa_ctx* ctx, Slot& sl, uint32_t C) {
+    if (C > sl.pair_cap || !sl.sb.keys[0]) {
         for (int i = 0; i < 2; i++) {
-            cudaFree(ctx->sb.keys[i]);
-            cudaFree(ctx->sb.vals[i]);
-            ctx->sb.keys[i] = nullptr;
-            ctx->sb.vals[i] = nullptr;
+            cudaFree(sl.sb.keys[i]);
+            cudaFree(sl.sb.vals[i]);
+            sl.sb.keys[i] = nullptr;
+            sl.sb.vals[i] = nullptr;
         }
         uint32_t cap = C + C / 4 + 4096;
         for (int i = 0; i < 2; i++) {
-            CU(cudaMalloc(&ctx->sb.keys[i], (size_t)cap * sizeof(skey_t)));
-            CU(cudaMalloc(&ctx->sb.vals[i], (size_t)cap * sizeof(uint32_t)));
+            CU(cudaMalloc(&sl.sb.keys[i], (size_t)cap * sizeof(skey_t)));
+            CU(cudaMalloc(&sl.sb.vals[i], (size_t)cap * sizeof(uint32_t)));
         }
-        ctx->pair_cap = cap;
-        if (!ctx->sb.hist) CU(cudaMalloc(&ctx->sb.hist, 256 * 8 * sizeof(uint32_t)));
-        if (!ctx->sb.tickets) CU(cudaMalloc(&ctx->sb.tickets, 8 * sizeof(uint32_t)));
+        sl.pair_cap = cap;
+        if (!sl.sb.hist) CU(cudaMalloc(&sl.sb.hist, 256 * 8 * sizeof(uint32_t)));
+        if (!sl.sb.tickets) CU(cudaMalloc(&sl.sb.tickets, 8 * sizeof(uint32_t)));
     }
-    size_t need = sort_state_words(ctx->pair_cap, 8);
-    CU(grow(ctx->sb.state, ctx->sort_state_cap, need));
+    size_t need = sort_state_words(sl.pair_cap, 8);
+    CU(grow(sl.sb.state, sl.sort_state_cap, need));
     // K2/K3 look-back state shares one buffer (K2 has finished when this grows)
-    size_t sneed = scan_state_words(ctx->vb_n) + (size_t)ctx->pair_cap / 2048 + 8;
-    CU(grow(ctx->vb.scan_state, ctx->scan_state_cap, sneed));
-    (void)passes;
+    size_t sneed = scan_state_words(sl.vb_n) + (size_t)sl.pair_cap / 2048 + 8;
+    CU(grow(sl.vb.scan_state, sl.scan_state_cap, sneed));
     return AAA_OK;
 }
 
-// Run the pipeline for one view into device buffers rgb (3 x out_h x W) / T.
-// stop_after: 1 = after K3 (unsorted pairs kept), 0 = full render.
+aaa_status ensure_out(aaa_ctx* ctx, Slot& sl, size_t floats) {
+    CU(grow(sl.d_out, sl.d_out_cap, floats));
+    return AAA_OK;
+}
+
+// Run the pipeline for one view in slot ctx->cur into device buffers rgb (3 x out_h x W) / T
+// (nullptr = the slot's staging image, copied to host_rgb / host_T on the raster stream).
+// stop_after: 1 = after K3 (unsorted pairs kept, nothing on the raster stream), 0 = full render.
 aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_end, float* rgb, float* T,
-                    bool debug_k1, int stop_after) {
-    cudaStream_t st = ctx->stream;
+                    float* host_rgb, float* host_T, bool debug_k1, int stop_after) {
+    Slot& sl = ctx->slot[ctx->cur];
+    cudaStream_t ps = ctx->pstream, rs = ctx->rstream;
     const int64_t n = ctx->scene.n;
     ViewParams vp = make_view(ctx, cam, row_begin, row_end);
-    aaa_status s = ensure_view_bufs(ctx, n);
+    // the slot's previous view must have left the raster stream before its buffers are reused
+    CU(cudaStreamWaitEvent(ps, sl.raster_done, 0));
+    aaa_status s = ensure_view_bufs(ctx, sl, n);
     if (s) return s;
-    s = ensure_tiles(ctx, vp.tiles_x * vp.tiles_y);
+    s = ensure_tiles(ctx, sl, vp.tiles_x * vp.tiles_y);
     if (s) return s;
-    if (debug_k1 && !ctx->vb.dbg) CU(cudaMalloc(&ctx->vb.dbg, (size_t)(n > 0 ? n : 1) * AAA_DBG_GAUSS_FIELDS * sizeof(double)));
-    CU(grow(ctx->vb.scan_state, ctx->scan_state_cap, scan_state_words(n) + 8));
+    if (debug_k1 && !sl.vb.dbg)
+        CU(cudaMalloc(&sl.vb.dbg, (size_t)(n > 0 ? n : 1) * AAA_DBG_GAUSS_FIELDS * sizeof(double)));
+    CU(grow(sl.vb.scan_state, sl.scan_state_cap, scan_state_words(n) + 8));
     const bool timing = (ctx->cfg.flags & AAA_FLAG_TIMING) != 0 && stop_after == 0;
     cudaEvent_t* ev = nullptr;
     if (timing) {
@@ -252,75 +286,109 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         }
         ev = ctx->ev_pool[ctx->ev_used++].data();
     }
-    auto mark = [&](int i) {
+    auto mark = [&](int i, cudaStream_t st) {
         if (ev) cudaEventRecord(ev[i], st);
     };
-    CU(cudaMemsetAsync(ctx->vb.counters, 0, CNT_TOTAL * sizeof(uint32_t), st));
+    CU(cudaMemsetAsync(sl.vb.counters, 0, CNT_TOTAL * sizeof(uint32_t), ps));
     size_t s2 = scan_state_words(n);
-    CU(cudaMemsetAsync(ctx->vb.scan_state, 0, s2 * sizeof(uint32_t), st));
-    mark(0);
-    launch_preprocess(ctx->scene, vp, ctx->vb, debug_k1, st);
-    mark(1);
+    CU(cudaMemsetAsync(sl.vb.scan_state, 0, s2 * sizeof(uint32_t), ps));
+    mark(0, ps);
+    launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
+    mark(1, ps);
     if (n > 0) ctx->launches += 2;
-    launch_scan(ctx->vb.counts, ctx->vb.offsets, n, &ctx->vb.counters[CNT_C], ctx->vb.scan_state,
-                &ctx->vb.counters[CNT_SCAN_TICKET], st);
+    launch_scan(sl.vb.counts, sl.vb.offsets, n, &sl.vb.counters[CNT_C], sl.vb.scan_state,
+                &sl.vb.counters[CNT_SCAN_TICKET], ps);
     CU(cudaGetLastError());
-    mark(2);
-    CU(cudaMemcpyAsync(ctx->h_counters, ctx->vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
+    mark(2, ps);
+    CU(cudaMemcpyAsync(ctx->h_counters, sl.vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ps));
+    CU(cudaStreamSynchronize(ps));
     const uint32_t C = ctx->h_counters[CNT_C];
     const int key_bits = 32;
-    s = ensure_pairs(ctx, C, sort_passes(key_bits));
+    s = ensure_pairs(ctx, sl, C);
     if (s) return s;
-    mark(3);
+    mark(3, ps);
     size_t emit_words = (size_t)C / 2048 + 2;
-    CU(cudaMemsetAsync(ctx->vb.scan_state, 0, emit_words * sizeof(uint32_t), st));
-    launch_cull_emit(vp, ctx->vb, n, C, ctx->sb.keys[0], ctx->sb.vals[0], ctx->vb.scan_state, st);
-    mark(4);
+    CU(cudaMemsetAsync(sl.vb.scan_state, 0, emit_words * sizeof(uint32_t), ps));
+    launch_cull_emit(vp, sl.vb, n, C, sl.sb.keys[0], sl.sb.vals[0], sl.vb.scan_state, ps);
+    mark(4, ps);
     if (C > 0) ctx->launches += 1;
-    ctx->last_vp = vp;
-    ctx->last_C = C;
-    ctx->last_key_bits = key_bits;
+    sl.vp = vp;
+    sl.C = C;
     if (stop_after == 1) {
-        ctx->last_sorted = 0;
+        sl.sorted = 0;
         CU(cudaGetLastError());
         return AAA_OK;
     }
-    int sorted = launch_sort(ctx->sb, &ctx->vb.counters[CNT_P], C, key_bits, st);
-    ctx->last_sorted = sorted;
-    mark(5);
-    launch_ranges(ctx->sb.keys[sorted], &ctx->vb.counters[CNT_P], C, ctx->ranges, vp.tiles_x * vp.tiles_y, vp.key_db,
-                  st);
-    mark(6);
+    int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_P], C, key_bits, ps);
+    sl.sorted = sorted;
+    mark(5, ps);
+    launch_ranges(sl.sb.keys[sorted], &sl.vb.counters[CNT_P], C, sl.ranges, vp.tiles_x * vp.tiles_y, vp.key_db, ps);
+    mark(6, ps);
     if (C > 0) ctx->launches += 3 + sort_passes(key_bits);
+    const int out_h = std::min(row_end * TILE, cam.height) - row_begin * TILE;
+    const size_t plane = (size_t)out_h * cam.width;
     RasterArgs ra{};
-    ra.keys = ctx->sb.keys[sorted];
-    ra.vals = ctx->sb.vals[sorted];
-    ra.ranges = ctx->ranges;
-    ra.raster = ctx->vb.raster;
-    ra.color = ctx->vb.color;
-    ra.out_rgb = rgb;
-    ra.out_T = T;
+    ra.keys = sl.sb.keys[sorted];
+    ra.vals = sl.sb.vals[sorted];
+    ra.ranges = sl.ranges;
+    ra.raster = sl.vb.raster;
+    ra.color = sl.vb.color;
+    if (!rgb || (!T && host_T)) {
+        s = ensure_out(ctx, sl, 4 * plane);
+        if (s) return s;
+    }
+    ra.out_rgb = rgb ? rgb : sl.d_out;
+    ra.out_T = T ? T : (host_T ? sl.d_out + 3 * plane : nullptr);
     ra.out_row0 = row_begin * TILE;
-    ra.out_h = std::min(row_end * TILE, cam.height) - row_begin * TILE;
+    ra.out_h = out_h;
     const int win_k = (ctx->cfg.flags & AAA_FLAG_FORCE_FALLBACK) ? 1 : ctx->cfg.window_k;
-    s = ensure_spill(ctx, (size_t)cam.width * cam.height, std::max(win_k, ctx->spill_k));
+    s = ensure_spill(ctx, sl, (size_t)cam.width * cam.height, std::max(win_k, sl.spill_k));
     if (s) return s;
-    ra.spill_hdr = ctx->spill_hdr;
-    ra.spill_e = ctx->spill_e;
-    ra.spill_cap = (uint32_t)ctx->spill_cap;
-    ra.spill_k = (uint32_t)ctx->spill_k;
-    ra.counters = ctx->vb.counters;
-    launch_raster(vp, ra, ctx->cfg.window_k, st);
-    mark(7);
-    launch_raster_fallback(vp, ra, st);
-    mark(8);
+    ra.spill_hdr = sl.spill_hdr;
+    ra.spill_e = sl.spill_e;
+    ra.spill_cap = (uint32_t)sl.spill_cap;
+    ra.spill_k = (uint32_t)sl.spill_k;
+    ra.counters = sl.vb.counters;
+    CU(cudaEventRecord(sl.prep_done, ps));
+    CU(cudaStreamWaitEvent(rs, sl.prep_done, 0));
+    mark(10, rs);
+    launch_raster(vp, ra, ctx->cfg.window_k, rs);
+    mark(7, rs);
+    launch_raster_fallback(vp, ra, rs);
+    mark(8, rs);
     if (vp.tile_row_end > vp.tile_row_begin) ctx->launches += 3;
+    if (host_rgb) CU(cudaMemcpyAsync(host_rgb, ra.out_rgb, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
+    if (host_T) CU(cudaMemcpyAsync(host_T, ra.out_T, plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
+    mark(9, rs);
+    CU(cudaEventRecord(sl.raster_done, rs));
     CU(cudaGetLastError());
     return AAA_OK;
 }
 
-aaa_status ensure_out(aaa_ctx* ctx, size_t floats) { CU(grow(ctx->d_out, ctx->d_out_cap, floats)); return AAA_OK; }
+// join the caller's stream: library streams start after the caller's prior work ...
+aaa_status enter(aaa_ctx* ctx) {
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaEventRecord(ctx->ev_entry, ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->pstream, ctx->ev_entry, 0));
+    CU(cudaStreamWaitEvent(ctx->rstream, ctx->ev_entry, 0));
+    return AAA_OK;
+}
+
+// ... and the caller's later work starts after everything the call enqueued
+aaa_status leave(aaa_ctx* ctx) {
+    CU(cudaEventRecord(ctx->ev_exit, ctx->rstream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_exit, 0));
+    CU(cudaEventRecord(ctx->ev_exit, ctx->pstream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_exit, 0));
+    return AAA_OK;
+}
+
+aaa_status sync_all(aaa_ctx* ctx) {
+    CU(cudaStreamSynchronize(ctx->pstream));
+    CU(cudaStreamSynchronize(ctx->rstream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return AAA_OK;
+}
 
 aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int row_begin, int row_end, float* rgb,
                          float* T) {
@@ -341,22 +409,34 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
     const size_t plane = (size_t)out_h * W;
     const bool dev_rgb = is_device_ptr(rgb);
     const bool dev_T = T ? is_device_ptr(T) : true;
-    if (!dev_rgb || !dev_T) {
-        aaa_status s = ensure_out(ctx, 4 * plane);
-        if (s) return s;
+    aaa_status s = enter(ctx);
+    if (s) return s;
+    for (int v = 0; v < n_views && !s; v++) {
+        ctx->cur ^= 1;
+        float* r = dev_rgb ? rgb + 3 * plane * v : nullptr;
+        float* t = T && dev_T ? T + plane * v : nullptr;
+        float* hr = dev_rgb ? nullptr : rgb + 3 * plane * v;
+        float* ht = T && !dev_T ? T + plane * v : nullptr;
+        s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0);
     }
-    for (int v = 0; v < n_views; v++) {
-        float* r = dev_rgb ? rgb + 3 * plane * v : ctx->d_out;
-        float* t = T ? (dev_T ? T + plane * v : ctx->d_out + 3 * plane) : nullptr;
-        aaa_status s = run_view(ctx, cams[v], row_begin, row_end, r, t, false, 0);
-        if (s) return s;
-        if (!dev_rgb) CU(cudaMemcpyAsync(rgb + 3 * plane * v, r, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-        if (T && !dev_T) CU(cudaMemcpyAsync(T + plane * v, t, plane * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-        if ((ctx->cfg.flags & AAA_FLAG_TIMING) && ctx->ev_used > 0)
-            CU(cudaEventRecord(ctx->ev_pool[ctx->ev_used - 1][9], ctx->stream));
-    }
-    if (!dev_rgb || !dev_T) CU(cudaStreamSynchronize(ctx->stream));
+    aaa_status s2 = leave(ctx);
+    if (s) return s;
+    if (s2) return s2;
+    if (!dev_rgb || !dev_T) return sync_all(ctx);
     return AAA_OK;
+}
+
+// run a view up to K3 (or K1 with the debug record) and wait for it
+aaa_status run_debug_view(aaa_ctx* ctx, bool debug_k1) {
+    const int ty = (ctx->cam.height + TILE - 1) / TILE;
+    aaa_status s = enter(ctx);
+    if (s) return s;
+    ctx->cur ^= 1;
+    s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, nullptr, nullptr, debug_k1, 1);
+    aaa_status s2 = leave(ctx);
+    if (s) return s;
+    if (s2) return s2;
+    return sync_all(ctx);
 }
 
 }  // namespace
@@ -372,15 +452,23 @@ aaa_status aaa_create(int32_t device, void* stream, aaa_ctx** out) {
     ctx->device = device;
     ctx->stream = (cudaStream_t)stream;
     aaa_default_config(&ctx->cfg);
+    auto bail = [&](cudaError_t e) {
+        cudaGetLastError();
+        aaa_destroy(ctx);
+        return e == cudaErrorMemoryAllocation ? AAA_ERR_OOM : AAA_ERR_CUDA;
+    };
     cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) {
-        delete ctx;
-        return AAA_ERR_CUDA;
-    }
-    e = cudaMallocHost(&ctx->h_counters, CNT_TOTAL * sizeof(uint32_t));
-    if (e != cudaSuccess) {
-        delete ctx;
-        return AAA_ERR_CUDA;
+    if (e != cudaSuccess) return bail(e);
+    if ((e = cudaMallocHost(&ctx->h_counters, CNT_TOTAL * sizeof(uint32_t))) != cudaSuccess) return bail(e);
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return bail(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->pstream, cudaStreamNonBlocking, hi)) != cudaSuccess) return bail(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->rstream, cudaStreamNonBlocking, lo)) != cudaSuccess) return bail(e);
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_entry, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_exit, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+    for (auto& sl : ctx->slot) {
+        if ((e = cudaEventCreateWithFlags(&sl.prep_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+        if ((e = cudaEventCreateWithFlags(&sl.raster_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
     }
     *out = ctx;
     return AAA_OK;
@@ -388,18 +476,18 @@ aaa_status aaa_create(int32_t device, void* stream, aaa_ctx** out) {
 
 void aaa_destroy(aaa_ctx* ctx) {
     if (!ctx) return;
-    cudaStreamSynchronize(ctx->stream);
+    if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
+    if (ctx->rstream) cudaStreamSynchronize(ctx->rstream);
     SceneDev& s = ctx->scene;
     cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
-    ViewBufs& vb = ctx->vb;
-    cudaFree(vb.cull); cudaFree(vb.raster); cudaFree(vb.color); cudaFree(vb.counts); cudaFree(vb.offsets);
-    cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
-    for (int i = 0; i < 2; i++) { cudaFree(ctx->sb.keys[i]); cudaFree(ctx->sb.vals[i]); }
-    cudaFree(ctx->sb.hist); cudaFree(ctx->sb.state); cudaFree(ctx->sb.tickets);
-    cudaFree(ctx->ranges); cudaFree(ctx->spill_hdr); cudaFree(ctx->spill_e); cudaFree(ctx->d_out);
+    for (auto& sl : ctx->slot) free_slot(sl);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev_pool)
         for (auto x : e) cudaEventDestroy(x);
+    if (ctx->ev_entry) cudaEventDestroy(ctx->ev_entry);
+    if (ctx->ev_exit) cudaEventDestroy(ctx->ev_exit);
+    if (ctx->pstream) cudaStreamDestroy(ctx->pstream);
+    if (ctx->rstream) cudaStreamDestroy(ctx->rstream);
     delete ctx;
 }
 
@@ -441,6 +529,10 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
         return fail(ctx, AAA_ERR_INVALID_ARG, "null scene array");
     if (g->n > MAX_GAUSSIANS) return fail(ctx, AAA_ERR_INVALID_ARG, "n too large (<= 2^24 Gaussians per context)");
     CU(cudaSetDevice(ctx->device));
+    {
+        aaa_status s = sync_all(ctx);  // views in flight still read the old scene
+        if (s) return s;
+    }
     cudaStream_t st = ctx->stream;
     SceneDev& s = ctx->scene;
     cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
@@ -486,7 +578,8 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
         if (tmp) cudaFree(tmp);
     }
     int64_t bad = INT64_MAX;
-    CU(cudaMemcpy(&bad, d_bad, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&bad, d_bad, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     cudaFree(d_bad);
     if (bad != INT64_MAX) {
         if (first_bad) *first_bad = bad;
@@ -534,27 +627,31 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
     if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
     const int ty = (ctx->cam.height + TILE - 1) / TILE;
     if (n_rows < ty) return fail(ctx, AAA_ERR_INVALID_ARG, "n_rows < tile rows");
-    aaa_status s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, false, 1);
+    aaa_status s = run_debug_view(ctx, false);
     if (s) return s;
+    const Slot& sl = ctx->slot[ctx->cur];
     uint32_t P = 0;
-    CU(cudaMemcpyAsync(&P, &ctx->vb.counters[CNT_P], sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(&P, &sl.vb.counters[CNT_P], sizeof(uint32_t), cudaMemcpyDeviceToHost));
     std::vector<skey_t> keys(P);
-    if (P) CU(cudaMemcpy(keys.data(), ctx->sb.keys[0], P * sizeof(skey_t), cudaMemcpyDeviceToHost));
+    if (P) CU(cudaMemcpy(keys.data(), sl.sb.keys[0], P * sizeof(skey_t), cudaMemcpyDeviceToHost));
     const int tx = (ctx->cam.width + TILE - 1) / TILE;
     for (int r = 0; r < n_rows; r++) out[r] = 0;
-    for (uint32_t i = 0; i < P; i++) out[(keys[i] >> ctx->last_vp.key_db) / tx]++;
+    for (uint32_t i = 0; i < P; i++) out[(keys[i] >> sl.vp.key_db) / tx]++;
     return AAA_OK;
 }
 
 aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     if (!ctx || !out) return AAA_ERR_INVALID_ARG;
-    CU(cudaStreamSynchronize(ctx->stream));
+    {
+        aaa_status s = sync_all(ctx);
+        if (s) return s;
+    }
     memset(out, 0, sizeof(*out));
     out->n = ctx->scene.n;
-    if (!ctx->vb.counters) return AAA_OK;
+    const Slot& sl = ctx->slot[ctx->cur];
+    if (!sl.vb.counters) return AAA_OK;
     uint32_t h[CNT_TOTAL];
-    CU(cudaMemcpy(h, ctx->vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(h, sl.vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
     out->visible = h[CNT_VISIBLE];
     out->candidates = h[CNT_C];
     out->pairs = h[CNT_P];
@@ -568,8 +665,8 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
 #endif
     out->launches = ctx->launches;
     // per-stage means over the timed views since the previous call
-    // stages: K1, K2, K3, sort, ranges, K6, K6b+K6c, host-sync gap, output copy, total
-    const int a[10] = {0, 1, 3, 4, 5, 6, 7, 2, 8, 0}, b[10] = {1, 2, 4, 5, 6, 7, 8, 3, 9, 9};
+    // stages: K1, K2, K3, sort, ranges, K6, K6s, host-sync gap, output copy, total
+    const int a[10] = {0, 1, 3, 4, 5, 10, 7, 2, 8, 0}, b[10] = {1, 2, 4, 5, 6, 7, 8, 3, 9, 9};
     double acc[10] = {0};
     int64_t nv = 0;
     for (size_t v = 0; v < ctx->ev_used; v++) {
@@ -589,42 +686,43 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
 
 aaa_status aaa_synchronize(aaa_ctx* ctx) {
     if (!ctx) return AAA_ERR_INVALID_ARG;
-    CU(cudaStreamSynchronize(ctx->stream));
-    return AAA_OK;
+    return sync_all(ctx);
 }
 
 aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, size_t* len) {
     if (!ctx || !dst || !len) return AAA_ERR_INVALID_ARG;
     if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
-    const int ty = (ctx->cam.height + TILE - 1) / TILE;
+    aaa_status s = AAA_OK;
+    if (what == AAA_DBG_GAUSS || what == AAA_DBG_KEYS_UNSORTED || what == AAA_DBG_VALS_UNSORTED)
+        s = run_debug_view(ctx, what == AAA_DBG_GAUSS);
+    else if (what >= AAA_DBG_GAUSS && what <= AAA_DBG_COLOR)
+        s = sync_all(ctx);
+    else
+        return fail(ctx, AAA_ERR_INVALID_ARG, "unknown debug buffer");
+    if (s) return s;
+    const Slot& sl = ctx->slot[ctx->cur];
+    if (!sl.vb.counters) return fail(ctx, AAA_ERR_STATE, "no view rendered yet");
     const void* src = nullptr;
     size_t bytes = 0;
-    aaa_status s = AAA_OK;
-    if (what == AAA_DBG_GAUSS) {
-        s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, true, 1);
-        src = ctx->vb.dbg;
-        bytes = (size_t)ctx->scene.n * AAA_DBG_GAUSS_FIELDS * sizeof(double);
-    } else if (what == AAA_DBG_KEYS_UNSORTED || what == AAA_DBG_VALS_UNSORTED) {
-        s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, false, 1);
-        src = what == AAA_DBG_KEYS_UNSORTED ? (const void*)ctx->sb.keys[0] : (const void*)ctx->sb.vals[0];
-    } else if (what == AAA_DBG_KEYS || what == AAA_DBG_VALS || what == AAA_DBG_RANGES || what == AAA_DBG_SPILL) {
-        src = what == AAA_DBG_KEYS ? (const void*)ctx->sb.keys[ctx->last_sorted]
-            : what == AAA_DBG_VALS ? (const void*)ctx->sb.vals[ctx->last_sorted]
-            : what == AAA_DBG_RANGES ? (const void*)ctx->ranges : (const void*)ctx->spill_hdr;
-    } else if (what == AAA_DBG_RASTER || what == AAA_DBG_COLOR) {
-        src = what == AAA_DBG_RASTER ? (const void*)ctx->vb.raster : (const void*)ctx->vb.color;
-        bytes = (size_t)ctx->scene.n * (what == AAA_DBG_RASTER ? RASTER_REC_F4 : 1) * sizeof(float4);
-    } else {
-        return fail(ctx, AAA_ERR_INVALID_ARG, "unknown debug buffer");
-    }
-    if (s) return s;
-    CU(cudaStreamSynchronize(ctx->stream));
     uint32_t h[CNT_TOTAL];
-    CU(cudaMemcpy(h, ctx->vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
-    if (what == AAA_DBG_KEYS || what == AAA_DBG_KEYS_UNSORTED) bytes = (size_t)h[CNT_P] * sizeof(skey_t);
-    if (what == AAA_DBG_VALS || what == AAA_DBG_VALS_UNSORTED) bytes = (size_t)h[CNT_P] * 4;
-    if (what == AAA_DBG_RANGES) bytes = (size_t)ctx->last_vp.tiles_x * ctx->last_vp.tiles_y * sizeof(uint2);
-    if (what == AAA_DBG_SPILL) bytes = (size_t)std::min((size_t)h[CNT_SPILL], ctx->spill_cap) * sizeof(SpillHdr);
+    CU(cudaMemcpy(h, sl.vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
+    switch (what) {
+        case AAA_DBG_GAUSS:
+            src = sl.vb.dbg;
+            bytes = (size_t)ctx->scene.n * AAA_DBG_GAUSS_FIELDS * sizeof(double);
+            break;
+        case AAA_DBG_KEYS_UNSORTED: src = sl.sb.keys[0]; bytes = (size_t)h[CNT_P] * sizeof(skey_t); break;
+        case AAA_DBG_VALS_UNSORTED: src = sl.sb.vals[0]; bytes = (size_t)h[CNT_P] * 4; break;
+        case AAA_DBG_KEYS: src = sl.sb.keys[sl.sorted]; bytes = (size_t)h[CNT_P] * sizeof(skey_t); break;
+        case AAA_DBG_VALS: src = sl.sb.vals[sl.sorted]; bytes = (size_t)h[CNT_P] * 4; break;
+        case AAA_DBG_RANGES: src = sl.ranges; bytes = (size_t)sl.vp.tiles_x * sl.vp.tiles_y * sizeof(uint2); break;
+        case AAA_DBG_SPILL:
+            src = sl.spill_hdr;
+            bytes = (size_t)std::min((size_t)h[CNT_SPILL], sl.spill_cap) * sizeof(SpillHdr);
+            break;
+        case AAA_DBG_RASTER: src = sl.vb.raster; bytes = (size_t)ctx->scene.n * RASTER_REC_F4 * sizeof(float4); break;
+        case AAA_DBG_COLOR: src = sl.vb.color; bytes = (size_t)ctx->scene.n * sizeof(float4); break;
+    }
     *len = bytes;
     if (bytes > cap) return fail(ctx, AAA_ERR_INVALID_ARG, "debug buffer too small");
     if (bytes && src) CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
