@@ -151,12 +151,27 @@ def test_bounds_and_tile_cull_match_oracle_qp(R, cfg):
     n_pix = 4096 if cfg == "c1" else 300
     pxs = rng.integers(0, cam.width, n_pix)
     pys = rng.integers(0, cam.height, n_pix)
+    # depth-key soundness (reading 23): the decoded key of (g, tile) is <= z* of g at every pixel of
+    # the tile where g contributes (the watermark certificate of K6 rests on it)
+    kdb = R.key_tile_shift()
+    code = (keys & np.uint32((1 << kdb) - 1)).astype(np.float64)
+    S_ = 2.0 ** kdb / 24.0
+    near_lo = float(np.float32(cam.near * (1 - 1e-5)))
+    if near_lo > cam.near * (1 - 1e-5):
+        near_lo = float(np.nextafter(np.float32(near_lo), np.float32(0)))
+    zdec = near_lo * np.exp2(code / S_)
+    key_of = dict(zip(zip(gidx.tolist(), tile.tolist()), zdec.tolist()))
+    n_checked = 0
     for x, y in zip(pxs, pys):
         c = orc.pixel_contribs(int(x), int(y))
         t = (y // 16) * tx + x // 16
         for row in c:
             if row[O.C_FIELDS.index("included")] > 0.5 and not (int(row[O.C_FIELDS.index("flags")]) & O.F_CUTOFF):
-                assert (int(row[O.C_FIELDS.index("g")]), int(t)) in emitted, (x, y, row)
+                gk = (int(row[O.C_FIELDS.index("g")]), int(t))
+                assert gk in emitted, (x, y, row)
+                assert key_of[gk] <= row[O.C_FIELDS.index("z")], (x, y, gk, key_of[gk], row[O.C_FIELDS.index("z")])
+                n_checked += 1
+    assert n_checked > 50
 
 
 # ------------------------------------------------------------------ sort + ranges
