@@ -660,8 +660,11 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     out->crossing = h[CNT_CROSS];
     out->evaluations = h[CNT_EVAL];
 #ifdef AAA_DEBUG_STATS
-    fprintf(stderr, "[aaa debug] shifts=%llu inserts=%llu\n", *(unsigned long long*)&h[20],
-            *(unsigned long long*)&h[22]);
+    {
+        const unsigned long long* u = reinterpret_cast<const unsigned long long*>(&h[20]);
+        fprintf(stderr, "[aaa debug] inserts=%llu shifts=%llu far_shifts=%llu sum_cnt=%llu ins_cnt16=%llu\n", u[0], u[1],
+                u[2], u[3], u[4]);
+    }
 #endif
     out->launches = ctx->launches;
     // per-stage means over the timed views since the previous call
