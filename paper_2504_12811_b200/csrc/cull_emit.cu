@@ -28,23 +28,36 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
     __shared__ uint32_t s_ticket, s_excl;
     __shared__ int64_t s_g0, s_g1;
     __shared__ uint32_t s_off[EMIT_SOFF];
-    if (threadIdx.x == 0) {
-        uint32_t t = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
-        s_ticket = t;
-        // the chunk's candidates [c0, c1] belong to Gaussians [g0, g1]: largest g with offset <= c
-        uint32_t c0 = t * EMIT_CHUNK, c1 = min(c0 + EMIT_CHUNK, C) - 1;
-        int64_t lo = 0, hi = n;
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (offsets[mid] <= c0) lo = mid; else hi = mid;
+    // per-thread emitted pairs, [item][thread] (a register array indexed in a rolled loop would
+    // live in local memory)
+    __shared__ skey_t s_key[EMIT_ITEMS][EMIT_THREADS];
+    __shared__ uint32_t s_val[EMIT_ITEMS][EMIT_THREADS];
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        // the chunk's candidates [c0, c1] belong to Gaussians [g0, g1] (largest g with offset <= c):
+        // two 17-ary searches side by side (half-warp each), one parallel load per step
+        const int lane = threadIdx.x, grp = lane >> 4, gi = lane & 15;
+        const uint32_t c0 = s_ticket * EMIT_CHUNK, c1 = min(c0 + EMIT_CHUNK, C) - 1;
+        const uint32_t target = grp ? c1 : c0;
+        int64_t lo = 0, hi = n;  // offsets[lo] <= target, answer in [lo, hi)
+        while (true) {
+            const bool active = hi - lo > 1;
+            if (!__any_sync(0xffffffffu, active)) break;
+            const int64_t step = (hi - lo + 16) / 17;
+            const int64_t pr = lo + (int64_t)(gi + 1) * step;
+            const bool le = active && pr < hi && offsets[pr] <= target;
+            const uint32_t bal = __ballot_sync(0xffffffffu, le);
+            const int k = __popc((bal >> (grp * 16)) & 0xFFFFu);
+            if (active) {
+                lo += (int64_t)k * step;
+                hi = min(hi, lo + step);
+            }
         }
-        s_g0 = lo;
-        hi = n;
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (offsets[mid] <= c1) lo = mid; else hi = mid;
+        if (gi == 0) {
+            if (grp) s_g1 = lo;
+            else s_g0 = lo;
         }
-        s_g1 = lo;
     }
     __syncthreads();
     const uint32_t chunk = s_ticket;
@@ -64,8 +77,6 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
         return lo;
     };
     int64_t g = find(cbeg, g0);
-    skey_t key[EMIT_ITEMS];
-    uint32_t val[EMIT_ITEMS];
     uint32_t keep_mask = 0, nkeep = 0;
     const bool no_cull = (vp.flags & AAA_FLAG_NO_TILE_CULL) != 0;
 #pragma unroll 1
@@ -110,8 +121,8 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
         }
         if (keep) {
             uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
-            key[k] = (tile << vp.key_db) | r.zkey;
-            val[k] = (uint32_t)g | (sub << VAL_INDEX_BITS);
+            s_key[k][threadIdx.x] = (tile << vp.key_db) | r.zkey;
+            s_val[k][threadIdx.x] = (uint32_t)g | (sub << VAL_INDEX_BITS);
             keep_mask |= 1u << k;
             nkeep++;
         }
@@ -127,8 +138,8 @@ __global__ void __launch_bounds__(EMIT_THREADS) k_cull_emit(ViewParams vp, const
 #pragma unroll
     for (int k = 0; k < EMIT_ITEMS; k++) {
         if (keep_mask & (1u << k)) {
-            keys[pos] = key[k];
-            vals[pos] = val[k];
+            keys[pos] = s_key[k][threadIdx.x];
+            vals[pos] = s_val[k][threadIdx.x];
             pos++;
         }
     }
