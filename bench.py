@@ -241,7 +241,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.empty_cache()
     H, W = views[0].height, views[0].width
     out = torch.empty((len(views), 3, H, W), dtype=torch.float32, device=dev)
-    R.set_config(flags=pkg.AAA_FLAG_TIMING, window_k=int(os.environ.get("AAA_WINDOW_K", "32")))
+    abl = {"none": 0, "no_cull": pkg.AAA_FLAG_NO_TILE_CULL, "no_hier": pkg.AAA_FLAG_NO_HIER_SORT}[args.ablation]
+    R.set_config(flags=pkg.AAA_FLAG_TIMING | abl, window_k=int(os.environ.get("AAA_WINDOW_K", "32")))
 
     def step():
         R.render_batch(views, out_rgb=out)
@@ -276,7 +277,7 @@ def run_ours(args, world, rank, local):
     value = total_views / (ms_max / 1000.0)
 
     # per-view counters (V, C, P, E) on a sample of this rank's views, timing off
-    R.set_config(flags=0)
+    R.set_config(flags=abl)
     samp = []
     for v in views[:: max(1, len(views) // 5)]:
         R.render(v, with_T=False)
@@ -361,7 +362,7 @@ def run_ours(args, world, rank, local):
                "data": "synthetic (seeded c3 generator; no datasets or trained weights exist offline)",
                "config": {"workload": f"{args.config}: 3M Gaussians SH3, 1920x1080, 200-view orbit; "
                                       f"{len(views)} views per rank per step",
-                          "views_per_rank_per_step": len(views), "gaussians": n, "width": W, "height": H,
+                          "views_per_rank_per_step": len(views), "ablation": args.ablation, "gaussians": n, "width": W, "height": H,
                           "parallelism": f"view-sharded x{world}", "l2": "inputs larger than L2 (720 MB scene "
                           "re-streamed per view), no flush"},
                "mpix_per_s": value * W * H / 1e6,
@@ -385,6 +386,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ablation", default="none", choices=["none", "no_cull", "no_hier"],
+                    help="Table 5 switches (P:521-523): no 3D tile culling / no per-pixel re-sort")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

@@ -98,7 +98,16 @@ typedef struct {
     float ms[10];
 } aaa_stats;
 
-enum { AAA_FLAG_TIMING = 1u, AAA_FLAG_NO_TILE_CULL = 2u, AAA_FLAG_FORCE_FALLBACK = 4u };
+/* aaa_config.flags:
+ *   AAA_FLAG_TIMING          per-stage CUDA events (read back by aaa_get_stats)
+ *   AAA_FLAG_NO_TILE_CULL    Table 5 "w/o culling": every tile of the bounds rect is kept
+ *                            (no 3D tile test, no sub-tile masks); the image is unchanged
+ *   AAA_FLAG_FORCE_FALLBACK  window K = 1: every pixel with two pending entries continues in the
+ *                            spill kernel (test of the exact continuation; the image is unchanged)
+ *   AAA_FLAG_NO_HIER_SORT    Table 5 "w/o hier. sort": blend in the global per-Gaussian
+ *                            order only — tile lists sorted by the view depth of the mean, no
+ *                            per-pixel re-sort (the image changes where that order is not z*) */
+enum { AAA_FLAG_TIMING = 1u, AAA_FLAG_NO_TILE_CULL = 2u, AAA_FLAG_FORCE_FALLBACK = 4u, AAA_FLAG_NO_HIER_SORT = 8u };
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */
 enum {

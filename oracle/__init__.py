@@ -44,7 +44,8 @@ class _Config(C.Structure):
     _fields_ = [("k", C.c_double), ("tau_mode", C.c_int32), ("tau_fixed", C.c_double),
                 ("alpha_max", C.c_double), ("T_eps", C.c_double), ("bg", C.c_double * 3),
                 ("band_rho", C.c_double), ("band_near", C.c_double), ("band_tie", C.c_double),
-                ("band_gauss", C.c_double)]
+                ("band_gauss", C.c_double), ("order_mode", C.c_int32), ("order_scale", C.c_double),
+                ("order_near", C.c_double), ("order_qmax", C.c_double)]
 
 
 _lib = None
@@ -80,7 +81,8 @@ def _ptr(a: np.ndarray):
 
 def default_config(**kw) -> dict:
     cfg = dict(k=0.3, tau_mode=0, tau_fixed=9.0, alpha_max=0.99, T_eps=1e-4, bg=(0.0, 0.0, 0.0),
-               band_rho=4e-3, band_near=1e-5, band_tie=4e-6, band_gauss=1e-5)
+               band_rho=4e-3, band_near=1e-5, band_tie=4e-6, band_gauss=1e-5,
+               order_mode=0, order_scale=1.0, order_near=1.0, order_qmax=0.0)
     cfg.update(kw)
     return cfg
 

@@ -49,6 +49,7 @@ struct Prepared {
     double Sinv[3][3]; // Sigma_hat^-1
     double radius;     // sqrt((tau + band_rho) * max shat)
     bool gauss_margin; // inside-test margin within band_gauss
+    double order_code; // order_mode 1: depth code of the mean (orc_config)
 };
 
 }  // namespace
@@ -195,6 +196,12 @@ void prepare_one(const orc_scene* s, int64_t g, Prepared& P) {
         for (int k = 0; k < K; k++) v += Y[k] * s->sh[(g * K + k) * 3 + c];
         P.rgb[c] = std::max(0.0, v + 0.5);
     }
+    // order_mode 1 (Table 5 "w/o hier. sort"): global order by the mean's view depth code
+    P.order_code = 0.0;
+    if (cfg.order_mode == 1) {
+        double u = cfg.order_scale * std::log2(std::max(P.muv[2], cfg.order_near) / cfg.order_near);
+        P.order_code = std::floor(std::min(std::max(u, 0.0), cfg.order_qmax));
+    }
     double lmax = std::max(P.shat[0], std::max(P.shat[1], P.shat[2]));
     P.radius = std::sqrt(std::max(0.0, P.tau + cfg.band_rho) * lmax);
 }
@@ -269,6 +276,13 @@ void pixel_contribs(const orc_scene* s, const std::vector<int64_t>* cand, int px
         c.flags = (near_rho ? ORC_F_CUTOFF : 0u) | (near_near ? ORC_F_NEAR : 0u) | (P.gauss_margin ? ORC_F_GAUSS : 0u);
         out.push_back(c);
     }
+    if (cfg.order_mode == 1) {  // global per-Gaussian order only (orc_config.order_mode)
+        std::sort(out.begin(), out.end(), [s](const Contrib& a, const Contrib& b) {
+            const double ca = s->prep[a.g].order_code, cb = s->prep[b.g].order_code;
+            return ca < cb || (ca == cb && a.g < b.g);
+        });
+        return;
+    }
     // exact per-ray order: ascending z*, ties by index (reading 4)
     std::sort(out.begin(), out.end(), [](const Contrib& a, const Contrib& b) {
         return a.z < b.z || (a.z == b.z && a.g < b.g);
@@ -281,9 +295,9 @@ void blend(const orc_scene* s, std::vector<Contrib>& cs, double* rgbT, uint32_t*
     double C[3] = {0, 0, 0}, T = 1.0;
     uint32_t f = 0;
     int nb = 0;
-    // tie flags among included neighbours
+    // tie flags among included neighbours; none in the global-order mode
     int prev = -1;
-    for (size_t i = 0; i < cs.size(); i++) {
+    for (size_t i = 0; i < cs.size() && cfg.order_mode == 0; i++) {
         if (!cs[i].included && !(cs[i].flags)) continue;
         if (prev >= 0) {
             double gap = (cs[i].z - cs[prev].z) / std::max(std::fabs(cs[prev].z), 1e-300);

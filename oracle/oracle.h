@@ -39,6 +39,13 @@ typedef struct {
     double band_near;  /* |z* - near| < band_near * max(1,z*)  (1e-5) */
     double band_tie;   /* (z_{k+1}-z_k)/z_k < band_tie          (4e-6) */
     double band_gauss; /* Gaussian-level margins, relative      (1e-5) */
+    /* blend order (Table 5 "w/o hier. sort"):
+     *   0: exact per-ray order by (z*, g) (reading 4)
+     *   1: the global per-Gaussian order only (3DGS-style sort by the view depth of the mean):
+     *      by (code, g), code = floor(clamp(order_scale * log2(max(mu_z, order_near) / order_near),
+     *      0, order_qmax)) — the depth code of the renderer's sort key */
+    int32_t order_mode;
+    double order_scale, order_near, order_qmax;
 } orc_config;
 
 /* per-Gaussian record exported by orc_gaussian (indices into out[]) */

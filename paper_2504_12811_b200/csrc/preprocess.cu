@@ -322,6 +322,10 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     const double u = vp.key_scale * log2(zlb * (1.0 - ZKEY_PAD) / vp.key_near);
     const double qmax = (double)((1u << vp.key_db) - 1u);
     uint32_t zkey = (uint32_t)fmin(fmax(floor(u), 0.0), qmax);
+    if (vp.flags & AAA_FLAG_NO_HIER_SORT) {  // Table 5 "w/o hier. sort": depth code of the mean
+        const double um = vp.key_scale * log2(fmax(muv[2], vp.key_near) / vp.key_near);
+        zkey = (uint32_t)fmin(fmax(floor(um), 0.0), qmax);
+    }
 
     // --- colour (reading 15): SH at d = (mu - o)/|mu - o|
     float rgb[3];

@@ -30,7 +30,9 @@ def _variants(c, cfg):
     # the oracle's tie flag (band_tie = 4e-6) marks a superset of those pixels
     TIGHT = min(cfg["band_tie"], 6e-7)  # 2 x the measured max FP32 z error (2.5e-7)
     clusters, cur = [], [seq[0]] if seq else []
-    for a, b in zip(seq[:-1], seq[1:]):
+    # global-order mode (Table 5 "w/o hier. sort"): the order is the key order, exact on both sides
+    pairs = zip(seq[:-1], seq[1:]) if cfg.get("order_mode", 0) == 0 else []
+    for a, b in pairs:
         if (z[b] - z[a]) / max(abs(z[a]), 1e-300) < TIGHT:
             cur.append(b)
         else:

@@ -452,3 +452,38 @@ def test_frustum_trivial_cases():
     far = orc.frustum_min_rho2([0], [(48.5, 63.5, 48.5, 63.5)])[0]
     # closest tile ray x=48.5 at depth 2: lateral offset (48.5-32)/56*2 = 0.589 -> rho^2 ~ (0.589/0.01)^2 * cos^2
     assert far > 1000
+
+
+def test_global_order_mode_equals_resorted_exact_contributions():
+    """order_mode 1 (Table 5 "w/o hier. sort"): the blend order is the depth code of each
+    Gaussian's view-space mean, then the index. Checked against the exact-mode contribution list
+    re-sorted in numpy by codes computed here from the scene and the camera."""
+    scene, cams = S.make_config("c1")
+    cam = cams[0]
+    kp = dict(order_mode=1, order_scale=2.0 ** 28 / 24.0, order_near=0.0099999, order_qmax=float(2 ** 28 - 1))
+    orc1 = O.Oracle(scene).set_view(cam, **kp)
+    orc0 = O.Oracle(scene).set_view(cam)
+    W = np.asarray(cam.world_to_view, dtype=np.float64).reshape(4, 4)
+    f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)
+    muz = f32(W[2, :3]) @ scene.means.astype(np.float64).T + float(np.float32(W[2, 3]))
+    u = kp["order_scale"] * np.log2(np.maximum(muz, kp["order_near"]) / kp["order_near"])
+    code = np.floor(np.clip(u, 0, kp["order_qmax"]))
+    CI = {f: i for i, f in enumerate(O.C_FIELDS)}
+    rng = np.random.default_rng(5)
+    n_diff = 0
+    for px, py in zip(rng.integers(0, cam.width, 300), rng.integers(0, cam.height, 300)):
+        c = orc0.pixel_contribs(int(px), int(py))
+        inc = c[c[:, CI["included"]] > 0.5]
+        g = inc[:, CI["g"]].astype(np.int64)
+        order = np.lexsort((g, code[g]))
+        T, C = 1.0, np.zeros(3)
+        for k in order:
+            a = inc[k, CI["alpha"]]
+            if T * (1 - a) < 1e-4:
+                break
+            C += a * inc[k, CI["r"]:CI["b"] + 1] * T
+            T *= 1 - a
+        ref, _, _ = orc1.render_pixels(np.array([px]), np.array([py]))
+        np.testing.assert_allclose(ref[0], [*C, T], rtol=0, atol=1e-12)
+        n_diff += int(not np.array_equal(order, np.argsort(inc[:, CI["z"]], kind="stable")))
+    assert n_diff > 0  # the two orders differ on some pixels of c1
