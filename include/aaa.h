@@ -167,6 +167,19 @@ aaa_status aaa_render_tiles(aaa_ctx* ctx, int32_t tile_row_begin, int32_t tile_r
  * Gaussian on each tile row), used to balance tile bands; out: ceil(H/16) int64. Syncs. */
 aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows);
 
+/* Training sampling frequency v_hat_train (Eq. 6): for every loaded
+ * Gaussian, the maximum over the cameras whose view frustum contains its mean of f / z, with z
+ * the mean's view depth and f = max(fx, fy) (reading 10). "Contains" is the culling frustum of
+ * reading 20 applied to the mean point: z >= near_z and the projection inside the pixel-centre
+ * rectangle [0.5, W - 0.5] x [0.5, H - 0.5]. +inf when no camera sees the mean or n_cams == 0
+ * (S:192). Computed in FP64 from the float32 inputs, rounded to float32.
+ * cams: n_cams host cameras (validated like aaa_set_camera). out: N floats, device or host
+ * pointer, nullable when store != 0. store != 0 also replaces the context's per-Gaussian
+ * v_train, so later renders use it (the next step of the pipeline).
+ * Errors: AAA_ERR_INVALID_ARG (n_cams < 0, bad camera, out null with store == 0),
+ * AAA_ERR_STATE (no scene loaded). Synchronises. */
+aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_cams, float* out, int32_t store);
+
 aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out); /* synchronises */
 aaa_status aaa_synchronize(aaa_ctx* ctx);
 

@@ -71,6 +71,7 @@ def lib():
         L.orc_sh_basis.argtypes = [P, P]
         L.orc_qp_min_norm.restype = C.c_double
         L.orc_qp_min_norm.argtypes = [C.c_int32, P, P]
+        L.orc_vtrain.argtypes = [P, C.c_int32, C.POINTER(_Camera), P, P]
         _lib = L
     return _lib
 
@@ -124,6 +125,21 @@ class Oracle:
         rc = lib().orc_set_view(self._h, C.byref(c), C.byref(k))
         assert rc == 0
         return self
+
+    def vtrain(self, cams):
+        """v_hat_train over cameras (Eq. 6): (values float64, boundary-ambiguity flags)."""
+        f32 = lambda v: float(np.float32(v))
+        arr = (_Camera * max(len(cams), 1))()
+        for i, cam in enumerate(cams):
+            c = arr[i]
+            c.width, c.height = int(cam.width), int(cam.height)
+            c.fx, c.fy, c.cx, c.cy = f32(cam.fx), f32(cam.fy), f32(cam.cx), f32(cam.cy)
+            c.world_to_view[:] = [f32(v) for v in np.asarray(cam.world_to_view, dtype=np.float64).reshape(16)]
+            c.near_z = f32(cam.near)
+        out = np.empty(self.n, dtype=np.float64)
+        amb = np.empty(self.n, dtype=np.int32)
+        assert lib().orc_vtrain(self._h, len(cams), arr, _ptr(out), _ptr(amb)) == 0
+        return out, amb.astype(bool)
 
     def gaussians(self) -> np.ndarray:
         out = np.empty((self.n, len(G_FIELDS)), dtype=np.float64)

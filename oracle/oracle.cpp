@@ -584,3 +584,36 @@ double orc_qp_min_norm(int32_t nc, const double* a, const double* b) {
 }
 
 }  // extern "C"
+
+// Eq. 6, frustum membership of the mean point as in S:154 with the culling frustum
+// of reading 20: near plane and the pixel-centre planes; f = max(fx, fy) (reading 10).
+int32_t orc_vtrain(const orc_scene* s, int32_t n_cams, const orc_camera* cams, double* out, int32_t* amb) {
+    const double INF = std::numeric_limits<double>::infinity();
+#pragma omp parallel for schedule(static)
+    for (int64_t g = 0; g < s->n; g++) {
+        const double* mu = &s->means[3 * g];
+        double best = -INF;
+        int32_t a = 0;
+        for (int32_t c = 0; c < n_cams; c++) {
+            const orc_camera& cam = cams[c];
+            const double* M = cam.world_to_view;
+            double v[3];
+            for (int i = 0; i < 3; i++) v[i] = M[4 * i] * mu[0] + M[4 * i + 1] * mu[1] + M[4 * i + 2] * mu[2] + M[4 * i + 3];
+            const double z = v[2];
+            const double eps = 1e-9;
+            if (std::fabs(z - cam.near_z) <= eps * std::max(1.0, std::fabs(z))) a = 1;
+            if (!(z >= cam.near_z)) continue;
+            const double px = cam.fx * v[0] / z + cam.cx, py = cam.fy * v[1] / z + cam.cy;
+            const double bx[2] = {0.5, cam.width - 0.5}, by[2] = {0.5, cam.height - 0.5};
+            for (int k = 0; k < 2; k++) {
+                if (std::fabs(px - bx[k]) <= eps * std::max(1.0, std::fabs(px))) a = 1;
+                if (std::fabs(py - by[k]) <= eps * std::max(1.0, std::fabs(py))) a = 1;
+            }
+            if (px < bx[0] || px > bx[1] || py < by[0] || py > by[1]) continue;
+            best = std::max(best, std::max(cam.fx, cam.fy) / z);
+        }
+        out[g] = best > 0 ? best : INF;
+        if (amb) amb[g] = a;
+    }
+    return 0;
+}

@@ -101,6 +101,13 @@ int32_t orc_frustum_min_rho2(const orc_scene* s, int64_t m, const int64_t* g, co
 void orc_sh_basis(const double* d, double* Y16);
 double orc_qp_min_norm(int32_t nc, const double* a, const double* b);
 
+/* v_hat_train (Eq. 6): out[g] = max over the cameras whose frustum
+ * contains the mean (view depth z >= near, projection inside the pixel-centre rectangle
+ * [0.5, W-0.5] x [0.5, H-0.5], reading 20) of max(fx, fy) / z; +inf if none. amb[g] = 1 when
+ * some camera's decision lies within a relative 1e-9 of a frustum boundary (FP rounding may flip
+ * it). Independent of the view set by orc_set_view. */
+int32_t orc_vtrain(const orc_scene* s, int32_t n_cams, const orc_camera* cams, double* out, int32_t* amb);
+
 #ifdef __cplusplus
 }
 #endif

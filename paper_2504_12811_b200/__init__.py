@@ -162,6 +162,18 @@ class Renderer:
         self.width, self.height = W, H
         return out_rgb, out_T
 
+    def compute_vtrain(self, cams, out=None, store: bool = False):
+        """v_hat_train of every loaded Gaussian over the training cameras (Eq. 6, aaa_compute_vtrain).
+        Returns a float32 CUDA tensor (or fills `out`); store=True also makes later renders use it."""
+        torch = self.torch
+        n = len(cams)
+        arr = (Camera * max(n, 1))(*[camera_struct(c) for c in cams])
+        if out is None:
+            out = torch.empty((self.n,), dtype=torch.float32, device=torch.device("cuda", self.device))
+        _check(self._ctx, lib().aaa_compute_vtrain(self._ctx, arr, n, C.c_void_p(out.data_ptr()), 1 if store else 0),
+               "aaa_compute_vtrain")
+        return out
+
     def render_tiles(self, row_begin: int, row_end: int, out_rgb=None, out_T=None):
         torch = self.torch
         H, W = self.height, self.width

@@ -145,6 +145,13 @@ struct RasterArgs {
     uint32_t* counters;
 };
 void launch_raster(const ViewParams& vp, const RasterArgs& ra, int window_k, cudaStream_t st);
+
+// v_hat_train cameras (Eq. 6): world->view rotation/translation, intrinsics, f = max(fx, fy)
+struct VtCam {
+    double R[9], t[3];
+    double fx, fy, cx, cy, near_z, f, w, h;
+};
+void launch_vtrain(const SceneDev& sc, const VtCam* cams, int n_cams, float* out, bool store, cudaStream_t st);
 void launch_raster_fallback(const ViewParams& vp, const RasterArgs& ra, cudaStream_t st);
 
 }  // namespace aaa

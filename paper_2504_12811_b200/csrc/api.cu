@@ -640,6 +640,46 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
     return AAA_OK;
 }
 
+aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_cams, float* out, int32_t store) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!ctx->loaded) return fail(ctx, AAA_ERR_STATE, "aaa_compute_vtrain before aaa_load_gaussians");
+    if (n_cams < 0 || (n_cams > 0 && !cams)) return fail(ctx, AAA_ERR_INVALID_ARG, "need n_cams >= 0 cameras");
+    if (!out && !store) return fail(ctx, AAA_ERR_INVALID_ARG, "out is null and store == 0");
+    std::vector<VtCam> h(n_cams > 0 ? n_cams : 1);
+    for (int i = 0; i < n_cams; i++) {
+        aaa_status s = check_camera(ctx, &cams[i]);
+        if (s) return s;
+        const aaa_camera& c = cams[i];
+        VtCam& v = h[i];
+        for (int r = 0; r < 3; r++) {
+            for (int k = 0; k < 3; k++) v.R[3 * r + k] = c.world_to_view[4 * r + k];
+            v.t[r] = c.world_to_view[4 * r + 3];
+        }
+        v.fx = c.fx; v.fy = c.fy; v.cx = c.cx; v.cy = c.cy; v.near_z = c.near_z;
+        v.f = std::max((double)c.fx, (double)c.fy);
+        v.w = c.width; v.h = c.height;
+    }
+    {
+        aaa_status s = sync_all(ctx);  // renders in flight still read v_train
+        if (s) return s;
+    }
+    cudaStream_t st = ctx->stream;
+    VtCam* d_cams = nullptr;
+    CU(cudaMalloc(&d_cams, h.size() * sizeof(VtCam)));
+    CU(cudaMemcpyAsync(d_cams, h.data(), h.size() * sizeof(VtCam), cudaMemcpyHostToDevice, st));
+    const size_t bytes = (size_t)ctx->scene.n * sizeof(float);
+    const bool dev_out = out && is_device_ptr(out);
+    float* d_out = dev_out ? out : nullptr;
+    if (out && !dev_out && bytes) CU(cudaMalloc(&d_out, bytes));
+    launch_vtrain(ctx->scene, d_cams, n_cams, d_out, store != 0, st);
+    CU(cudaGetLastError());
+    if (out && !dev_out && bytes) CU(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (out && !dev_out) cudaFree(d_out);
+    cudaFree(d_cams);
+    return AAA_OK;
+}
+
 aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     if (!ctx || !out) return AAA_ERR_INVALID_ARG;
     {

@@ -487,3 +487,56 @@ def test_global_order_mode_equals_resorted_exact_contributions():
         np.testing.assert_allclose(ref[0], [*C, T], rtol=0, atol=1e-12)
         n_diff += int(not np.array_equal(order, np.argsort(inc[:, CI["z"]], kind="stable")))
     assert n_diff > 0  # the two orders differ on some pixels of c1
+
+
+def test_vtrain_spec_examples():
+    """Eq. 6 and SPEC S:151-159 worked examples: one camera, f = 800, mean at depth 4
+    on screen -> 200; cameras at depths 4 and 2 both seeing the mean -> 400; empty list -> +inf
+    (S:192); a camera that does not see the mean (behind / off screen) does not count."""
+    sc = one_gaussian((0.0, 0.0, 0.0), (0.1, 0.1, 0.1))
+    orc = O.Oracle(sc)
+
+    def cam_at(depth, W=800, H=600, f=800.0, shift=0.0):
+        V = np.eye(4)
+        V[2, 3] = depth           # world origin at view depth `depth`
+        V[0, 3] = shift           # lateral offset in view space
+        return pinhole(W, H, f, V)
+    v, amb = orc.vtrain([cam_at(4.0)])
+    assert v[0] == 200.0 and not amb[0]
+    v, _ = orc.vtrain([cam_at(4.0), cam_at(2.0)])
+    assert v[0] == 400.0
+    v, _ = orc.vtrain([])
+    assert np.isinf(v[0])
+    v, _ = orc.vtrain([cam_at(-1.0), cam_at(4.0, shift=10.0)])   # behind; projects to x = 2400 > W
+    assert np.isinf(v[0])
+    v, _ = orc.vtrain([cam_at(4.0, f=600.0), cam_at(8.0, W=1600, f=1600.0)])
+    assert v[0] == 200.0   # max(600/4, 1600/8)
+    # anamorphic: f = max(fx, fy) (reading 10)
+    c = cam_at(4.0)
+    c = S.Camera(c.width, c.height, 800.0, 1200.0, c.cx, c.cy, c.world_to_view, c.near)
+    v, _ = orc.vtrain([c])
+    assert v[0] == 300.0
+
+
+def test_vtrain_brute_force_on_c1():
+    """orc_vtrain against a direct numpy evaluation of the same definition on c1 x 3 cameras."""
+    scene, cams = S.make_config("c1")
+    cl = [cams[0], cams[0].scaled(fx=40.0, fy=40.0), pinhole(64, 64, 56.0, np.diag([1.0, 1.0, 1.0, 1.0]) @ np.eye(4))]
+    orc = O.Oracle(scene)
+    v, amb = orc.vtrain(cl)
+    mu = scene.means.astype(np.float64)
+    best = np.full(len(mu), -np.inf)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    for c in cl:
+        M = f32(np.asarray(c.world_to_view, np.float64))
+        p = mu @ M[:3, :3].T + M[:3, 3]
+        z = p[:, 2]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            px = float(np.float32(c.fx)) * p[:, 0] / z + float(np.float32(c.cx))
+            py = float(np.float32(c.fy)) * p[:, 1] / z + float(np.float32(c.cy))
+        ok = (z >= float(np.float32(c.near))) & (px >= 0.5) & (px <= c.width - 0.5) & (py >= 0.5) & (py <= c.height - 0.5)
+        best = np.where(ok, np.maximum(best, max(float(np.float32(c.fx)), float(np.float32(c.fy))) / np.where(ok, z, 1)), best)
+    want = np.where(best > 0, best, np.inf)
+    m = ~amb
+    np.testing.assert_allclose(v[m], want[m], rtol=1e-14)
+    assert np.isfinite(v).sum() > 10 and np.isinf(v).sum() > 0
