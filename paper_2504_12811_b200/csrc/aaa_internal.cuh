@@ -42,6 +42,8 @@ struct ViewParams {
     double key_near;       // near_lo (encode base, = key_near_f promoted)
     float key_inv_scale_f; // 1/S rounded down (decode)
     float key_near_f;      // near_lo rounded down (decode)
+    double inv_fx, inv_fy; // 1/fx, 1/fy
+    double key_zmul;       // (1 - ZKEY_PAD) / key_near (encode)
 };
 
 // Scene residency (L0): structure of float4 arrays, 16-byte aligned.

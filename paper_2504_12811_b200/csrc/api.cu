@@ -164,6 +164,9 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     float is = (float)(1.0 / vp.key_scale);
     if ((double)is > 1.0 / vp.key_scale) is = std::nextafter(is, 0.f);
     vp.key_inv_scale_f = is;
+    vp.inv_fx = 1.0 / vp.fx;
+    vp.inv_fy = 1.0 / vp.fy;
+    vp.key_zmul = (1.0 - ZKEY_PAD) / vp.key_near;
     return vp;
 }
 

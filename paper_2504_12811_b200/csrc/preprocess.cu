@@ -125,7 +125,8 @@ __device__ bool axis_bounds(double s_ii, double s_i3, double s33, double disc, d
     // cancellation-free form, tan r2 = s_ii / (s_i3 +- sqrt(D)).
     double n1 = rhypot(num, s33), n2 = rhypot(s_ii, num);
     double d1x = num * n1, d1y = s33 * n1, d2x = s_ii * n2, d2y = num * n2;
-    double mx = mu_i / mn, my = mu_z / mn;  // v(theta_mu)
+    const double imn = 1.0 / mn;
+    double mx = mu_i * imn, my = mu_z * imn;  // v(theta_mu)
     // rotation step (Eq. 16, reading 16): representative of each root in (theta_mu - pi, theta_mu]
     // <=> sin(theta_mu - r) >= 0 <=> cross(v(theta_mu), v(r)) >= 0
     if (mx * d1y - my * d1x < 0.0) { d1x = -d1x; d1y = -d1y; }
@@ -174,14 +175,16 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     double vhat = muv[2] > 0.0 ? f / muv[2] : INF;
     double veff = fmin((double)B4.w, vhat);
     double cf = isinf(veff) ? 0.0 : (double)vp.k / (veff * veff);
-    double shat[3], sig[3];
+    double shat[3], sig[3], isig[3];
     for (int i = 0; i < 3; i++) {
         shat[i] = s[i] * s[i] + cf;
         sig[i] = sqrt(shat[i]);
+        isig[i] = rsqrt(shat[i]);
     }
     double d[3] = {mu[0] - vp.o[0], mu[1] - vp.o[1], mu[2] - vp.o[2]};
     double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    for (int i = 0; i < 3; i++) d[i] /= dn;
+    const double idn = 1.0 / dn;
+    for (int i = 0; i < 3; i++) d[i] *= idn;
     double Amp = 1.0;
     if (cf > 0.0) {  // Eq. 12 with d' = R^T d (Eq. 11)
         double dp0 = R[0] * d[0] + R[3] * d[1] + R[6] * d[2];
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
         for (int j = 0; j < 3; j++) M[3 * i + j] = Q[3 * i + j] * sig[j];
     double Wm[9];
     for (int j = 0; j < 3; j++)
-        for (int i = 0; i < 3; i++) Wm[3 * j + i] = Q[3 * i + j] / sig[j];
+        for (int i = 0; i < 3; i++) Wm[3 * j + i] = Q[3 * i + j] * isig[j];
     double c[3];
     mat3_vec(Wm, muv, c);
     for (int i = 0; i < 3; i++) c[i] = -c[i];
@@ -275,12 +278,12 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     prx = prx_f;
     pry = pry_f;
     // pixel ray r(p) = ((px-cx)/fx, (py-cy)/fy, 1); unit-space direction w(p) = W r(p) is affine in p
-    double rref[3] = {(prx - vp.cx) / vp.fx, (pry - vp.cy) / vp.fy, 1.0};
+    double rref[3] = {(prx - vp.cx) * vp.inv_fx, (pry - vp.cy) * vp.inv_fy, 1.0};
     double wref[3], wa[3], wb[3];
     mat3_vec(Wm, rref, wref);
     for (int j = 0; j < 3; j++) {
-        wa[j] = Wm[3 * j + 0] / vp.fx;
-        wb[j] = Wm[3 * j + 1] / vp.fy;
+        wa[j] = Wm[3 * j + 0] * vp.inv_fx;
+        wb[j] = Wm[3 * j + 1] * vp.inv_fy;
     }
     // rho^2(p) = |c x w(p)|^2 / |w(p)|^2,  c x w(p) = F0 + dx E1 + dy E2 (re-centred, DESIGN K6)
     double F0[3], E1[3], E2[3];
@@ -313,13 +316,14 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
 
     // --- depth key: tight lower bound of z* over every contributing ray (reading 23)
     double cn = sqrt(c2);
-    double ch[3] = {c[0] / cn, c[1] / cn, c[2] / cn};
+    const double icn = 1.0 / cn;
+    double ch[3] = {c[0] * icn, c[1] * icn, c[2] * icn};
     double gc = dot3(gz, ch);
     double gp[3] = {gz[0] - gc * ch[0], gz[1] - gc * ch[1], gz[2] - gc * ch[2]};
-    double zlb = muv[2] - sqrt(tau) * sqrt(dot3(gp, gp)) - (tau / cn) * fmax(0.0, -gc);
+    double zlb = muv[2] - sqrt(tau) * sqrt(dot3(gp, gp)) - (tau * icn) * fmax(0.0, -gc);
     zlb = fmax(zlb, vp.near_z);
     // log-depth code, rounded down (decode <= z_lb (1 - pad)); zlb >= near > near_lo keeps u >= 0
-    const double u = vp.key_scale * log2(zlb * (1.0 - ZKEY_PAD) / vp.key_near);
+    const double u = vp.key_scale * log2(zlb * vp.key_zmul);
     const double qmax = (double)((1u << vp.key_db) - 1u);
     uint32_t zkey = (uint32_t)fmin(fmax(floor(u), 0.0), qmax);
     if (vp.flags & AAA_FLAG_NO_HIER_SORT) {  // Table 5 "w/o hier. sort": depth code of the mean
