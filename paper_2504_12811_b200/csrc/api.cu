@@ -1,13 +1,14 @@
 // api.cu — the C ABI (include/aaa.h): context, scene residency, per-view pipeline driver.
 //
 // Pipeline per view:
-//   prep stream:   K1 preprocess -> K2 scan -> [one 16-byte D2H of the counters, the only host
-//                  sync] -> K3 cull+emit -> K4 onesweep sort -> K5 ranges
-//   raster stream: K6 raster -> K6s spill resolution -> (host outputs) D2H image copy
-// Every per-view buffer lives in one of two slots used alternately, so view v+1's K1-K5 run on
-// the (high-priority) prep stream while view v's K6/K6s still occupy the (low-priority) raster
-// stream; the events prep_done / raster_done of a slot order the two streams. Both streams are
-// library-owned and non-blocking; the caller's stream is joined at entry and exit of each call.
+//   compute stream: K1 preprocess -> K2 scan -> [one 16-byte D2H of the counters, the only host
+//                   sync] -> K3 cull+emit -> K4 onesweep sort -> K5 ranges -> K6 raster -> K6s
+//   copy stream:    (host outputs) D2H of the image, overlapping the next view's kernels
+// Every per-view buffer lives in one of two slots used alternately; the events prep_done /
+// raster_done of a slot order the two streams. (Running view v+1's K1-K5 concurrently with view
+// v's K6 on a second compute stream was measured 1% slower on c3: every stage is latency-bound
+// and they only contend.) Both streams are library-owned and non-blocking; the caller's stream is
+// joined at entry and exit of each call.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -49,7 +50,7 @@ struct Slot {
 struct aaa_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;             // caller's stream
-    cudaStream_t pstream = nullptr, rstream = nullptr;  // prep (high priority) / raster (low priority)
+    cudaStream_t pstream = nullptr, rstream = nullptr;  // compute / image-copy streams
     cudaEvent_t ev_entry = nullptr, ev_exit = nullptr;
     aaa_config cfg{};
     aaa_camera cam{};
@@ -65,8 +66,7 @@ struct aaa_ctx {
     int64_t launches = 0;
 };
 
-// prep stream:   e0 K1 e1 K2 e2 [sync] e3 K3 e4 sort e5 ranges e6
-// raster stream: e10 K6 e7 K6s e8 [copy] e9
+// compute stream: e0 K1 e1 K2 e2 [sync] e3 K3 e4 sort e5 ranges e6 | e10 K6 e7 K6s e8 | [copy] e9
 constexpr int N_EV = 11;
 
 namespace {
@@ -352,18 +352,24 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.spill_cap = (uint32_t)sl.spill_cap;
     ra.spill_k = (uint32_t)sl.spill_k;
     ra.counters = sl.vb.counters;
-    CU(cudaEventRecord(sl.prep_done, ps));
-    CU(cudaStreamWaitEvent(rs, sl.prep_done, 0));
-    mark(10, rs);
-    launch_raster(vp, ra, ctx->cfg.window_k, rs);
-    mark(7, rs);
-    launch_raster_fallback(vp, ra, rs);
-    mark(8, rs);
+    mark(10, ps);
+    launch_raster(vp, ra, ctx->cfg.window_k, ps);
+    mark(7, ps);
+    launch_raster_fallback(vp, ra, ps);
+    mark(8, ps);
     if (vp.tile_row_end > vp.tile_row_begin) ctx->launches += 3;
-    if (host_rgb) CU(cudaMemcpyAsync(host_rgb, ra.out_rgb, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
-    if (host_T) CU(cudaMemcpyAsync(host_T, ra.out_T, plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
-    mark(9, rs);
-    CU(cudaEventRecord(sl.raster_done, rs));
+    if (host_rgb || host_T) {
+        // image D2H on the copy stream, overlapping the next view's kernels
+        CU(cudaEventRecord(sl.prep_done, ps));
+        CU(cudaStreamWaitEvent(rs, sl.prep_done, 0));
+        if (host_rgb) CU(cudaMemcpyAsync(host_rgb, ra.out_rgb, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
+        if (host_T) CU(cudaMemcpyAsync(host_T, ra.out_T, plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
+        mark(9, rs);
+        CU(cudaEventRecord(sl.raster_done, rs));
+    } else {
+        mark(9, ps);
+        CU(cudaEventRecord(sl.raster_done, ps));
+    }
     CU(cudaGetLastError());
     return AAA_OK;
 }
