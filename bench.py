@@ -241,7 +241,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.empty_cache()
     H, W = views[0].height, views[0].width
     out = torch.empty((len(views), 3, H, W), dtype=torch.float32, device=dev)
-    abl = {"none": 0, "no_cull": pkg.AAA_FLAG_NO_TILE_CULL, "no_hier": pkg.AAA_FLAG_NO_HIER_SORT}[args.ablation]
+    abl = {"none": 0, "no_cull": pkg.AAA_FLAG_NO_TILE_CULL, "no_hier": pkg.AAA_FLAG_NO_HIER_SORT,
+           "no_3d": pkg.AAA_FLAG_NO_3D}[args.ablation]
     R.set_config(flags=pkg.AAA_FLAG_TIMING | abl, window_k=int(os.environ.get("AAA_WINDOW_K", "32")))
 
     def step():
@@ -386,8 +387,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ablation", default="none", choices=["none", "no_cull", "no_hier"],
-                    help="Table 5 switches (P:521-523): no 3D tile culling / no per-pixel re-sort")
+    ap.add_argument("--ablation", default="none", choices=["none", "no_cull", "no_hier", "no_3d"],
+                    help="Table 5 switches (P:521-524): no 3D tile culling / no per-pixel re-sort / 2D splats")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

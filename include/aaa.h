@@ -106,8 +106,20 @@ typedef struct {
  *                            spill kernel (test of the exact continuation; the image is unchanged)
  *   AAA_FLAG_NO_HIER_SORT    Table 5 "w/o hier. sort": blend in the global per-Gaussian
  *                            order only — tile lists sorted by the view depth of the mean, no
- *                            per-pixel re-sort (the image changes where that order is not z*) */
-enum { AAA_FLAG_TIMING = 1u, AAA_FLAG_NO_TILE_CULL = 2u, AAA_FLAG_FORCE_FALLBACK = 4u, AAA_FLAG_NO_HIER_SORT = 8u };
+ *                            per-pixel re-sort (the image changes where that order is not z*)
+ *   AAA_FLAG_NO_3D           Table 5 "w/o 3D": affine 2D splat evaluation (EWA projection
+ *                            J Sigma_hat_view J^T of the filtered Gaussian, J the perspective
+ *                            Jacobian at the mean; rho^2 = d^T Sigma'^-1 d), exact 2D tile culling,
+ *                            the global mean-depth order (implies NO_HIER_SORT); Gaussians whose
+ *                            mean is closer than near are dropped, no camera-inside test.
+ *                            With NO_TILE_CULL and k = 0 this is a 3DGS-style baseline path. */
+enum {
+    AAA_FLAG_TIMING = 1u,
+    AAA_FLAG_NO_TILE_CULL = 2u,
+    AAA_FLAG_FORCE_FALLBACK = 4u,
+    AAA_FLAG_NO_HIER_SORT = 8u,
+    AAA_FLAG_NO_3D = 16u
+};
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */
 enum {

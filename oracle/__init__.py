@@ -45,7 +45,7 @@ class _Config(C.Structure):
                 ("alpha_max", C.c_double), ("T_eps", C.c_double), ("bg", C.c_double * 3),
                 ("band_rho", C.c_double), ("band_near", C.c_double), ("band_tie", C.c_double),
                 ("band_gauss", C.c_double), ("order_mode", C.c_int32), ("order_scale", C.c_double),
-                ("order_near", C.c_double), ("order_qmax", C.c_double)]
+                ("order_near", C.c_double), ("order_qmax", C.c_double), ("eval_mode", C.c_int32)]
 
 
 _lib = None
@@ -83,7 +83,7 @@ def _ptr(a: np.ndarray):
 def default_config(**kw) -> dict:
     cfg = dict(k=0.3, tau_mode=0, tau_fixed=9.0, alpha_max=0.99, T_eps=1e-4, bg=(0.0, 0.0, 0.0),
                band_rho=4e-3, band_near=1e-5, band_tie=4e-6, band_gauss=1e-5,
-               order_mode=0, order_scale=1.0, order_near=1.0, order_qmax=0.0)
+               order_mode=0, order_scale=1.0, order_near=1.0, order_qmax=0.0, eval_mode=0)
     cfg.update(kw)
     return cfg
 

@@ -50,6 +50,9 @@ struct Prepared {
     double radius;     // sqrt((tau + band_rho) * max shat)
     bool gauss_margin; // inside-test margin within band_gauss
     double order_code; // order_mode 1: depth code of the mean (orc_config)
+    double pm[2];      // eval_mode 1: projected mean (pixels)
+    double conic[3];   // eval_mode 1: Sigma'^-1 = [[c0, c1], [c1, c2]]
+    double radius2d;   // eval_mode 1: sqrt((tau + band) lambda_max(Sigma')) (exact reject radius)
 };
 
 }  // namespace
@@ -196,6 +199,42 @@ void prepare_one(const orc_scene* s, int64_t g, Prepared& P) {
         for (int k = 0; k < K; k++) v += Y[k] * s->sh[(g * K + k) * 3 + c];
         P.rgb[c] = std::max(0.0, v + 0.5);
     }
+    // eval_mode 1 (Table 5 "w/o 3D"): EWA projection Sigma' = J (Rv Sigma_hat Rv^T) J^T
+    if (cfg.eval_mode == 1) {
+        M3 Sv;
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) {
+                double v = 0;
+                for (int a = 0; a < 3; a++)
+                    for (int b = 0; b < 3; b++) v += s->Rv[i][a] * Shat[a][b] * s->Rv[j][b];
+                Sv[i][j] = v;
+            }
+        const double x = P.muv[0], y = P.muv[1], z = P.muv[2];
+        const double J[2][3] = {{cam.fx / z, 0.0, -cam.fx * x / (z * z)}, {0.0, cam.fy / z, -cam.fy * y / (z * z)}};
+        double S2[2][2];
+        for (int i = 0; i < 2; i++)
+            for (int j = 0; j < 2; j++) {
+                double v = 0;
+                for (int a = 0; a < 3; a++)
+                    for (int b = 0; b < 3; b++) v += J[i][a] * Sv[a][b] * J[j][b];
+                S2[i][j] = v;
+            }
+        const double det = S2[0][0] * S2[1][1] - S2[0][1] * S2[1][0];
+        P.conic[0] = S2[1][1] / det;
+        P.conic[1] = -S2[0][1] / det;
+        P.conic[2] = S2[0][0] / det;
+        P.pm[0] = cam.fx * x / z + cam.cx;
+        P.pm[1] = cam.fy * y / z + cam.cy;
+        const double hm = 0.5 * (S2[0][0] + S2[1][1]), hd = 0.5 * (S2[0][0] - S2[1][1]);
+        const double lmax2 = hm + std::sqrt(hd * hd + S2[0][1] * S2[0][1]);
+        P.radius2d = std::sqrt(std::max(0.0, P.tau + cfg.band_rho) * lmax2);
+        // 3DGS mean-frustum rule (reading 36): projected mean within 1.3x the image about its centre
+        const bool in_fr = std::fabs(P.pm[0] - 0.5 * cam.width) <= 0.65 * cam.width &&
+                           std::fabs(P.pm[1] - 0.5 * cam.height) <= 0.65 * cam.height;
+        P.valid = (P.tau > 0) && (z >= cam.near_z) && det > 0 && in_fr;
+        P.inside = false;
+        P.gauss_margin = false;
+    }
     // order_mode 1 (Table 5 "w/o hier. sort"): global order by the mean's view depth code
     P.order_code = 0.0;
     if (cfg.order_mode == 1) {
@@ -247,6 +286,24 @@ void pixel_contribs(const orc_scene* s, const std::vector<int64_t>* cand, int px
     for (int64_t i = 0; i < m; i++) {
         int64_t g = cand ? (*cand)[i] : i;
         const Prepared& P = s->prep[g];
+        if (cfg.eval_mode == 1) {  // affine 2D splat (Table 5 "w/o 3D")
+            if (!P.valid) continue;
+            const double dx = px + 0.5 - P.pm[0], dy = py + 0.5 - P.pm[1];
+            const double rho2 = P.conic[0] * dx * dx + 2.0 * P.conic[1] * dx * dy + P.conic[2] * dy * dy;
+            const bool in_rho = rho2 < P.tau, near_rho = std::fabs(rho2 - P.tau) < cfg.band_rho;
+            if (!in_rho && !near_rho) continue;
+            Contrib c;
+            c.z = P.muv[2];
+            c.rho2 = rho2;
+            c.tau = P.tau;
+            c.alpha = std::min(cfg.alpha_max, P.oA * std::exp(-0.5 * rho2));
+            for (int k = 0; k < 3; k++) c.rgb[k] = P.rgb[k];
+            c.g = g;
+            c.included = in_rho;
+            c.flags = near_rho ? ORC_F_CUTOFF : 0u;
+            out.push_back(c);
+            continue;
+        }
         if (!(P.tau > 0) || (P.inside && !P.gauss_margin)) continue;
         if (use_rejects) {  // exact sphere-vs-line reject (rho^2 >= dist^2 / lambda_max)
             double d[3] = {P.mu[0] - s->o[0], P.mu[1] - s->o[1], P.mu[2] - s->o[2]};
@@ -349,6 +406,13 @@ void tile_candidates(const orc_scene* s, int tx, int ty, std::vector<int64_t>& o
     out.clear();
     for (int64_t g = 0; g < s->n; g++) {
         const Prepared& P = s->prep[g];
+        if (s->cfg.eval_mode == 1) {  // 2D splat: disc (projected mean, radius) vs the tile rectangle
+            if (!P.valid) continue;
+            const double qx = std::min(std::max(P.pm[0], x0), x1), qy = std::min(std::max(P.pm[1], y0), y1);
+            const double ddx = qx - P.pm[0], ddy = qy - P.pm[1];
+            if (ddx * ddx + ddy * ddy <= P.radius2d * P.radius2d * (1.0 + 1e-9)) out.push_back(g);
+            continue;
+        }
         if (!(P.tau > 0) || (P.inside && !P.gauss_margin)) continue;
         double d[3] = {P.mu[0] - s->o[0], P.mu[1] - s->o[1], P.mu[2] - s->o[2]};
         double dl = std::sqrt(dot3(d, d));

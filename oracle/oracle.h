@@ -46,6 +46,11 @@ typedef struct {
      *      0, order_qmax)) — the depth code of the renderer's sort key */
     int32_t order_mode;
     double order_scale, order_near, order_qmax;
+    /* evaluation (Table 5 "w/o 3D"): 0: 3D maximum-response evaluation;
+     * 1: affine 2D splat — Sigma' = J Sigma_hat_view J^T with the perspective Jacobian J at the
+     *    mean, rho^2 = d^T Sigma'^-1 d, d = pixel centre - projected mean; a Gaussian whose mean
+     *    is closer than near is dropped; no camera-inside test (use with order_mode 1) */
+    int32_t eval_mode;
 } orc_config;
 
 /* per-Gaussian record exported by orc_gaussian (indices into out[]) */

@@ -149,6 +149,125 @@ __device__ bool axis_bounds(double s_ii, double s_i3, double s33, double disc, d
 }
 
 // ------------------------------------------------------------------ K1
+// Table 5 "w/o 3D" (AAA_FLAG_NO_3D): the affine 2D splat of the filtered Gaussian.
+// Sigma' = J (M M^T) J^T, J the perspective Jacobian at the mean (EWA); the cull record carries
+// the exact 2D quadratic q(d) = d^T Sigma'^-1 d - tau around the projected mean, so K3's box
+// minimum performs exact 2D tile / sub-tile culling; the key is the mean-depth code.
+// (A separate kernel, so the 3D K1's register allocation is untouched; its prelude — filter,
+// amplitude, tau — is the same arithmetic as K1's.)
+__global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams vp, ViewBufs vb) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= sc.n) return;
+    const float4 A4 = __ldg(&sc.geomA[g]), B4 = __ldg(&sc.geomB[g]), C4 = __ldg(&sc.geomC[g]);
+    vb.counts[g] = 0;
+    const double mu[3] = {A4.x, A4.y, A4.z};
+    const double s[3] = {B4.x, B4.y, B4.z};
+    double R[9];
+    quat_to_rot(C4, R);
+    double muv[3];
+    mat3_vec(vp.Rv, mu, muv);
+    for (int i = 0; i < 3; i++) muv[i] += vp.tv[i];
+    const double f = fmax(vp.fx, vp.fy);
+    const double vhat = muv[2] > 0.0 ? f / muv[2] : CUDART_INF;
+    const double veff = fmin((double)B4.w, vhat);
+    const double cf = isinf(veff) ? 0.0 : (double)vp.k / (veff * veff);
+    double shat[3], sig[3];
+    for (int i = 0; i < 3; i++) {
+        shat[i] = s[i] * s[i] + cf;
+        sig[i] = sqrt(shat[i]);
+    }
+    double d[3] = {mu[0] - vp.o[0], mu[1] - vp.o[1], mu[2] - vp.o[2]};
+    const double idn = 1.0 / sqrt(dot3(d, d));
+    for (int i = 0; i < 3; i++) d[i] *= idn;
+    double Amp = 1.0;
+    if (cf > 0.0) {  // Eq. 12 with d' = R^T d (Eq. 11)
+        const double dp0 = R[0] * d[0] + R[3] * d[1] + R[6] * d[2];
+        const double dp1 = R[1] * d[0] + R[4] * d[1] + R[7] * d[2];
+        const double dp2 = R[2] * d[0] + R[5] * d[1] + R[8] * d[2];
+        const double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+        const double num = dp0 * dp0 * s2[1] * s2[2] + dp1 * dp1 * s2[0] * s2[2] + dp2 * dp2 * s2[0] * s2[1];
+        const double den = dp0 * dp0 * shat[1] * shat[2] + dp1 * dp1 * shat[0] * shat[2] + dp2 * dp2 * shat[0] * shat[1];
+        Amp = sqrt(num / den);
+    }
+    const double oA = (double)A4.w * Amp;
+    double tau = 2.0 * log(255.0 * oA);
+    if (vp.tau_mode == 1) tau = fmin((double)vp.tau_fixed, tau);
+    if (!(tau > 0.0)) return;
+    double Q[9], M[9];
+    mat3_mul(vp.Rv, R, Q);
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) M[3 * i + j] = Q[3 * i + j] * sig[j];
+
+    const double x = muv[0], y = muv[1], z = muv[2];
+    if (!(z >= vp.near_z)) return;
+    // 3DGS mean-frustum rule: the projected mean within 1.3x the image about its centre
+    {
+        const double pmx = vp.fx * x / z + vp.cx, pmy = vp.fy * y / z + vp.cy;
+        if (fabs(pmx - 0.5 * vp.width) > 0.65 * vp.width || fabs(pmy - 0.5 * vp.height) > 0.65 * vp.height) return;
+    }
+    double S[9];  // view-space covariance M M^T
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) S[3 * i + j] = dot3(&M[3 * i], &M[3 * j]);
+    const double iz = 1.0 / z;
+    const double J0[3] = {vp.fx * iz, 0.0, -vp.fx * x * iz * iz}, J1[3] = {0.0, vp.fy * iz, -vp.fy * y * iz * iz};
+    double SJ0[3], SJ1[3];
+    mat3_vec(S, J0, SJ0);
+    mat3_vec(S, J1, SJ1);
+    const double a = dot3(J0, SJ0), b = dot3(J0, SJ1), c = dot3(J1, SJ1);
+    const double det = a * c - b * b;
+    if (!(det > 0.0)) return;
+    const double ca = c / det, cb = -b / det, cc = a / det;  // conic Sigma'^-1
+    const double hm = 0.5 * (a + c), hd = 0.5 * (a - c);
+    const double r = sqrt(tau * (hm + sqrt(hd * hd + b * b)));
+    const double pmx = vp.fx * x * iz + vp.cx, pmy = vp.fy * y * iz + vp.cy;
+    const double PAD = 1.0;
+    const double ixlo = ceil(fmax(pmx - r - PAD - 0.5, -1.0)), ixhi = floor(fmin(pmx + r + PAD - 0.5, (double)vp.width));
+    const double iylo = ceil(fmax(pmy - r - PAD - 0.5, -1.0)), iyhi = floor(fmin(pmy + r + PAD - 0.5, (double)vp.height));
+    const int i0 = max(0, (int)ixlo), i1 = min(vp.width - 1, (int)ixhi);
+    const int j0 = max(0, (int)iylo), j1 = min(vp.height - 1, (int)iyhi);
+    if (i0 > i1 || j0 > j1) return;
+    const float prx_f = (float)pmx, pry_f = (float)pmy;
+    const double prx = prx_f, pry = pry_f;
+    // q relative to p_ref = the f32-rounded projected mean: d = p - p_ref + e, e = p_ref - pm
+    const double ex = prx - pmx, ey = pry - pmy;
+    double qd = ca * ex + cb * ey, qe = cb * ex + cc * ey;
+    double qf = ca * ex * ex + 2.0 * cb * ex * ey + cc * ey * ey - tau;
+    const double px0 = i0 + 0.5, px1 = i1 + 0.5, py0 = j0 + 0.5, py1 = j1 + 0.5;
+    if (!(quad_box_min(ca, cb, cc, qd, qe, qf, px0 - prx, px1 - prx, py0 - pry, py1 - pry) < 0.0)) return;
+    int tx0 = i0 / TILE, tx1 = i1 / TILE, ty0 = j0 / TILE, ty1 = j1 / TILE;
+    ty0 = max(ty0, vp.tile_row_begin);
+    ty1 = min(ty1, vp.tile_row_end - 1);
+    const double qmax = (double)((1u << vp.key_db) - 1u);
+    const double um = vp.key_scale * log2(fmax(z, vp.key_near) / vp.key_near);
+    const uint32_t zkey = (uint32_t)fmin(fmax(floor(um), 0.0), qmax);
+    float rgb[3];
+    sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
+    CullRec cu;
+    cu.qa = ca; cu.qb = cb; cu.qc = cc; cu.qd = qd; cu.qe = qe; cu.qf = qf;
+    cu.ia = 1.0 / ca;
+    cu.ic = 1.0 / cc;
+    const double dq = ca * cc - cb * cb;
+    cu.xs = (cb * qe - cc * qd) / dq;
+    cu.ys = (cb * qd - ca * qe) / dq;
+    cu.qi = (ca * cu.xs + 2.0 * cb * cu.ys + 2.0 * qd) * cu.xs + (cc * cu.ys + 2.0 * qe) * cu.ys + qf;
+    cu.pref_x = prx_f;
+    cu.pref_y = pry_f;
+    cu.tx0 = (uint16_t)tx0; cu.ty0 = (uint16_t)ty0; cu.tx1 = (uint16_t)tx1; cu.ty1 = (uint16_t)ty1;
+    cu.i0 = (uint16_t)i0; cu.j0 = (uint16_t)j0; cu.i1 = (uint16_t)i1; cu.j1 = (uint16_t)j1;
+    cu.cross_slot = -1;
+    cu.zkey = zkey;
+    vb.cull[g] = cu;
+    // raster record (2D): [p_ref, oA, tau], [conic a, b, c, e.x], [e.y, -, -, -]
+    float4* rr = vb.raster + g * RASTER_REC_F4;
+    rr[0] = make_float4(prx_f, pry_f, (float)oA, (float)tau);
+    rr[1] = make_float4((float)ca, (float)cb, (float)cc, (float)ex);
+    rr[2] = make_float4((float)ey, 0.f, 0.f, 0.f);
+    vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+    const uint32_t cnt = (ty0 <= ty1) ? (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1) : 0u;
+    vb.counts[g] = cnt;
+    atomicAdd(&vb.counters[CNT_VISIBLE], 1u);
+}
+
 #ifndef AAA_K1_MINB
 #define AAA_K1_MINB 3  // 168 registers: 3 CTAs of 128 threads per SM (A/B: 0.78 -> 0.69 ms on c3)
 #endif
@@ -397,7 +516,10 @@ void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, b
     if (sc.n == 0) return;
     int threads = 128;
     unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
-    k_preprocess<<<blocks, threads, 0, st>>>(sc, vp, vb, debug ? 1 : 0);
+    if (vp.flags & AAA_FLAG_NO_3D)
+        k_preprocess_2d<<<blocks, threads, 0, st>>>(sc, vp, vb);
+    else
+        k_preprocess<<<blocks, threads, 0, st>>>(sc, vp, vb, debug ? 1 : 0);
 }
 
 }  // namespace aaa

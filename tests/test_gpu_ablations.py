@@ -76,3 +76,33 @@ def test_no_hier_sort_matches_oracle_global_order(R, cfg, view):
     assert rep["ok"], rep
     if cfg == "c2":  # the ablation really changes the order somewhere (else the test proves nothing)
         assert np.abs(img - exact).max() > 1e-2
+
+
+@pytest.mark.parametrize("cfg,view", [("c1", 0), ("c2", 0), ("c2", 77)])
+def test_no_3d_matches_oracle_2d_splat(R, cfg, view):
+    """Table 5 "w/o 3D": affine 2D splat evaluation in the global mean-depth order, against
+    the oracle's eval_mode 1 (EWA Sigma' = J Sigma_v J^T, pinned on CPU)."""
+    scene, cams = S.make_config(cfg)
+    cam = cams[view]
+    R.load(scene)
+    try:
+        R.set_config(flags=pkg.AAA_FLAG_NO_3D)
+        img = _img(R, cam)
+        R.set_camera(cam)
+        kp = _key_params(R, cam)
+    finally:
+        R.set_config(flags=0)
+    orc = O.Oracle(scene).set_view(cam, eval_mode=1, **kp)
+    yy, xx = np.mgrid[0:cam.height, 0:cam.width]
+    rep = compare(orc, img.reshape(-1, 4), xx.ravel(), yy.ravel())
+    assert rep["ok"], rep
+    # 2D tile culling is exact: without it the image is the same up to FP32 cutoff decisions
+    # (K3 tests the FP64 conic, K6 evaluates the FP32-rounded one), i.e. it passes the same bar
+    try:
+        R.set_config(flags=pkg.AAA_FLAG_NO_3D | pkg.AAA_FLAG_NO_TILE_CULL)
+        img2 = _img(R, cam)
+    finally:
+        R.set_config(flags=0)
+    rep2 = compare(orc, img2.reshape(-1, 4), xx.ravel(), yy.ravel())
+    assert rep2["ok"], rep2
+    assert (np.abs(img - img2).max(axis=2) > 0).mean() < 1e-3

@@ -540,3 +540,52 @@ def test_vtrain_brute_force_on_c1():
     m = ~amb
     np.testing.assert_allclose(v[m], want[m], rtol=1e-14)
     assert np.isfinite(v).sum() > 10 and np.isinf(v).sum() > 0
+
+
+def test_2d_splat_mode_closed_form_and_jacobian():
+    """eval_mode 1 (Table 5 "w/o 3D"): rho^2 = d^T (J Sigma_v J^T)^-1 d with J the Jacobian
+    of the pinhole projection at the mean. (a) On-axis isotropic Gaussian: rho^2 = z^2 |d|^2 /
+    (f sigma)^2 in closed form. (b) An anisotropic off-axis Gaussian: J by central differences of
+    the projection x -> (fx X/Z + cx, fy Y/Z + cy) in numpy."""
+    cfg = dict(order_mode=1, order_scale=1.0, order_near=0.01, order_qmax=0.0, eval_mode=1, k=0.0)
+    cam = pinhole(64, 64, 56.0)
+    sig, z = 0.3, 3.0
+    sc = one_gaussian((0.0, 0.0, z), (sig, sig, sig), o=0.8)
+    orc = O.Oracle(sc).set_view(cam, **cfg)
+    CI = {f: i for i, f in enumerate(O.C_FIELDS)}
+    for px, py in ((32, 32), (36, 30), (40, 41)):
+        c = orc.pixel_contribs(px, py)
+        d = np.array([px + 0.5 - 32.0, py + 0.5 - 32.0])
+        s32, z32 = float(np.float32(sig)), float(np.float32(z))
+        want = z32 * z32 * (d @ d) / (56.0 * s32) ** 2
+        assert c.shape[0] == 1
+        np.testing.assert_allclose(c[0, CI["rho2"]], want, rtol=1e-12)
+    # (b)
+    q = np.array([0.9, 0.2, -0.3, 0.25]); q /= np.linalg.norm(q)
+    mu, s = np.array([0.4, -0.3, 2.5]), np.array([0.25, 0.05, 0.12])
+    sc = one_gaussian(tuple(mu), tuple(s), q=tuple(q), o=0.9)
+    orc = O.Oracle(sc).set_view(cam, **cfg)
+    mu32 = sc.means[0].astype(np.float64)
+    qq = sc.quats[0].astype(np.float64); qq /= np.linalg.norm(qq)
+    w, x, y, zq = qq
+    R = np.array([[1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y)],
+                  [2 * (x * y + w * zq), 1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x)],
+                  [2 * (x * zq - w * y), 2 * (y * zq + w * x), 1 - 2 * (x * x + y * y)]])
+    Sv = R @ np.diag(sc.scales[0].astype(np.float64) ** 2) @ R.T
+    proj = lambda p: np.array([56.0 * p[0] / p[2] + 32.0, 56.0 * p[1] / p[2] + 32.0])
+    h = 1e-6
+    Jn = np.stack([(proj(mu32 + h * e) - proj(mu32 - h * e)) / (2 * h) for e in np.eye(3)], 1)
+    C2 = np.linalg.inv(Jn @ Sv @ Jn.T)
+    pm = proj(mu32)
+    n_hit = 0
+    for px in range(40, 56, 3):
+        for py in range(10, 40, 3):
+            c = orc.pixel_contribs(px, py)
+            d = np.array([px + 0.5, py + 0.5]) - pm
+            want = d @ C2 @ d
+            if c.shape[0]:
+                np.testing.assert_allclose(c[0, CI["rho2"]], want, rtol=1e-6)
+                n_hit += 1
+            else:
+                assert want > orc.gaussians()[0, O.G_FIELDS.index("tau")] - 1e-3
+    assert n_hit > 3
