@@ -118,7 +118,10 @@ enum {
     AAA_FLAG_NO_TILE_CULL = 2u,
     AAA_FLAG_FORCE_FALLBACK = 4u,
     AAA_FLAG_NO_HIER_SORT = 8u,
-    AAA_FLAG_NO_3D = 16u
+    AAA_FLAG_NO_3D = 16u,
+    AAA_FLAG_SAVE_CONTRIBS = 32u  /* aaa_render records each pixel's blended contributions (in blend
+                                   * order) for aaa_render_backward; single full-image default renders
+                                   * only; the call synchronises */
 };
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */
@@ -191,6 +194,19 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows);
  * Errors: AAA_ERR_INVALID_ARG (n_cams < 0, bad camera, out null with store == 0),
  * AAA_ERR_STATE (no scene loaded). Synchronises. */
 aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_cams, float* out, int32_t store);
+
+/* Backward pass (the paper trains with this rasterizer): gradients of
+ * a scalar loss L through the last aaa_render made with AAA_FLAG_SAVE_CONTRIBS (full image, no
+ * ablation flags). In (device float32): dL_drgb 3 x H x W, dL_dT H x W (nullable = 0). Out
+ * (device float32, overwritten): d_means N x 3, d_scales N x 3, d_quats N x 4 (w.r.t. the raw,
+ * unnormalised input quaternion), d_opac N, d_sh N x (deg+1)^2 x 3 (the load layout). The blend
+ * order and the contribution set of the forward are held fixed (the tau cutoff, near plane,
+ * culling and early termination carry no derivative); v_train is not differentiated.
+ * Errors: AAA_ERR_STATE (no saved render, or the scene/camera changed since), AAA_ERR_INVALID_ARG
+ * (null pointers), AAA_ERR_CUDA. The saving render sizes its per-pixel record to the largest
+ * blend count (re-rendering once when it grows). Synchronises. */
+aaa_status aaa_render_backward(aaa_ctx* ctx, const float* dL_drgb, const float* dL_dT, float* d_means,
+                               float* d_scales, float* d_quats, float* d_opac, float* d_sh);
 
 aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out); /* synchronises */
 aaa_status aaa_synchronize(aaa_ctx* ctx);

@@ -14,7 +14,7 @@ import numpy as np
 
 from ._abi import (AAA_DBG_GAUSS, AAA_DBG_GAUSS_FIELDS, AAA_DBG_KEYS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_SPILL,
                    AAA_DBG_RANGES, AAA_DBG_VALS, AAA_DBG_VALS_UNSORTED, AAA_FLAG_FORCE_FALLBACK,
-                   AAA_FLAG_NO_3D, AAA_FLAG_NO_HIER_SORT, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_TIMING, AaaError, Camera, Config, Gaussians, Stats, lib,
+                   AAA_FLAG_NO_3D, AAA_FLAG_NO_HIER_SORT, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_SAVE_CONTRIBS, AAA_FLAG_TIMING, AaaError, Camera, Config, Gaussians, Stats, lib,
                    EXPORTED_SYMBOLS)
 
 __all__ = ["Renderer", "lib", "Camera", "Config", "Gaussians", "Stats", "AaaError", "camera_struct",
@@ -111,6 +111,7 @@ class Renderer:
             raise AaaError(st, f"aaa_load_gaussians: first bad Gaussian {bad.value}: "
                                f"{lib().aaa_last_error(self._ctx).decode()}", first_bad=bad.value)
         self.n = g.n
+        self.sh_degree = int(g.sh_degree)
 
     def set_camera(self, cam) -> None:
         c = camera_struct(cam)
@@ -172,6 +173,23 @@ class Renderer:
             out = torch.empty((self.n,), dtype=torch.float32, device=torch.device("cuda", self.device))
         _check(self._ctx, lib().aaa_compute_vtrain(self._ctx, arr, n, C.c_void_p(out.data_ptr()), 1 if store else 0),
                "aaa_compute_vtrain")
+        return out
+
+    def backward(self, dL_drgb, dL_dT=None):
+        """Gradients of a scalar loss through the last render made with AAA_FLAG_SAVE_CONTRIBS
+        (aaa_render_backward). Returns dict of CUDA tensors: means, scales, quats, opacities, sh."""
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        dL_drgb = dL_drgb.contiguous().float()
+        dT = dL_dT.contiguous().float() if dL_dT is not None else None
+        K = (self.sh_degree + 1) ** 2
+        out = dict(means=torch.empty((self.n, 3), device=dev), scales=torch.empty((self.n, 3), device=dev),
+                   quats=torch.empty((self.n, 4), device=dev), opacities=torch.empty((self.n,), device=dev),
+                   sh=torch.empty((self.n, K, 3), device=dev))
+        p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p()
+        _check(self._ctx, lib().aaa_render_backward(self._ctx, p(dL_drgb), p(dT), p(out["means"]), p(out["scales"]),
+                                                    p(out["quats"]), p(out["opacities"]), p(out["sh"])),
+               "aaa_render_backward")
         return out
 
     def render_tiles(self, row_begin: int, row_end: int, out_rgb=None, out_T=None):

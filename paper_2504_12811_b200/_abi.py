@@ -7,6 +7,7 @@ from pathlib import Path
 _LIB_PATH = Path(__file__).resolve().parent / "libaaa.so"
 
 AAA_FLAG_TIMING, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_FORCE_FALLBACK, AAA_FLAG_NO_HIER_SORT, AAA_FLAG_NO_3D = 1, 2, 4, 8, 16
+AAA_FLAG_SAVE_CONTRIBS = 32
 (AAA_DBG_GAUSS, AAA_DBG_KEYS, AAA_DBG_VALS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_VALS_UNSORTED, AAA_DBG_RANGES,
  AAA_DBG_SPILL, AAA_DBG_RASTER, AAA_DBG_COLOR) = range(9)
 AAA_DBG_GAUSS_FIELDS = 26
@@ -14,7 +15,7 @@ AAA_DBG_GAUSS_FIELDS = 26
 EXPORTED_SYMBOLS = ["aaa_version", "aaa_create", "aaa_destroy", "aaa_set_stream", "aaa_default_config",
                     "aaa_set_config", "aaa_load_gaussians", "aaa_set_camera", "aaa_render", "aaa_render_batch",
                     "aaa_render_tiles", "aaa_tile_row_costs", "aaa_get_stats", "aaa_synchronize",
-                    "aaa_debug_copy", "aaa_last_error", "aaa_compute_vtrain"]
+                    "aaa_debug_copy", "aaa_last_error", "aaa_compute_vtrain", "aaa_render_backward"]
 
 
 class AaaError(RuntimeError):
@@ -77,6 +78,7 @@ def lib(path: Path | None = None):
         L.aaa_synchronize.argtypes = [V]
         L.aaa_debug_copy.argtypes = [V, I32, V, C.c_size_t, C.POINTER(C.c_size_t)]
         L.aaa_compute_vtrain.argtypes = [V, C.POINTER(Camera), I32, V, I32]
+        L.aaa_render_backward.argtypes = [V, V, V, V, V, V, V, V]
         L.aaa_last_error.argtypes = [V]
         L.aaa_last_error.restype = C.c_char_p
         for f in EXPORTED_SYMBOLS:

@@ -8,7 +8,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaaa.so"
-SOURCES = ["preprocess.cu", "scan.cu", "cull_emit.cu", "sort.cu", "raster.cu", "vtrain.cu", "api.cu"]
+SOURCES = ["preprocess.cu", "scan.cu", "cull_emit.cu", "sort.cu", "raster.cu", "vtrain.cu", "backward.cu", "api.cu"]
 HEADERS = ["aaa_internal.cuh", "geom.cuh", "lookback.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -145,8 +145,32 @@ struct RasterArgs {
     uint32_t spill_cap;
     uint32_t spill_k;
     uint32_t* counters;
+    // backward support (AAA_FLAG_SAVE_CONTRIBS): every blended contribution of pixel p, in blend
+    // order, as (g bits, alpha) at rec[p * rec_cap + i]; rec_n[p] = count (may exceed rec_cap:
+    // overflow, reported by the backward pass). Null when not saving.
+    float2* rec;
+    uint32_t* rec_n;
+    uint32_t rec_cap;
 };
 void launch_raster(const ViewParams& vp, const RasterArgs& ra, int window_k, cudaStream_t st);
+
+// backward pass (backward.cu): per-Gaussian accumulators of dL/dc (3), dL/dW (9, row-major
+// W[j][i]), dL/doA (1), dL/drgb (3)
+constexpr int BWD_ACC = 16;
+struct BwdArgs {
+    const float2* rec;      // recorded blends (RasterArgs::rec)
+    const uint32_t* rec_n;
+    uint32_t rec_cap;
+    const float* dL_drgb;   // 3 x H x W
+    const float* dL_dT;     // H x W (nullable)
+    const float4* raster;   // the view's raster records
+    const float4* color;
+    float* acc;             // N x BWD_ACC
+    uint32_t* overflow;     // pixels whose record overflowed
+    float *d_means, *d_scales, *d_quats, *d_opac, *d_sh;
+};
+void launch_backward(const SceneDev& sc, const ViewParams& vp, const BwdArgs& ba, cudaStream_t st);
+void launch_max_u32(const uint32_t* a, size_t n, uint32_t* out, cudaStream_t st);
 
 // v_hat_train cameras (Eq. 6): world->view rotation/translation, intrinsics, f = max(fx, fy)
 struct VtCam {

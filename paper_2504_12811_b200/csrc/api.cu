@@ -64,7 +64,18 @@ struct aaa_ctx {
     std::vector<std::vector<cudaEvent_t>> ev_pool;
     size_t ev_used = 0;
     int64_t launches = 0;
+    // backward support (AAA_FLAG_SAVE_CONTRIBS): the last single-view render's blend records
+    float2* rec = nullptr;
+    size_t rec_cap_px = 0;  // pixels x entries the record buffer holds
+    uint32_t rec_cap = 256; // recorded blends per pixel (grown when a render needs more)
+    uint32_t* rec_n = nullptr;
+    bool saved = false;     // rec holds the render of slot `cur`
+    float* bwd_acc = nullptr;
+    size_t bwd_acc_cap = 0;
+    uint32_t* bwd_overflow = nullptr;
 };
+
+
 
 // compute stream: e0 K1 e1 K2 e2 [sync] e3 K3 e4 sort e5 ranges e6 | e10 K6 e7 K6s e8 | [copy] e9
 constexpr int N_EV = 11;
@@ -352,6 +363,23 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.spill_cap = (uint32_t)sl.spill_cap;
     ra.spill_k = (uint32_t)sl.spill_k;
     ra.counters = sl.vb.counters;
+    if (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) {
+        const size_t npx = (size_t)cam.width * cam.height;
+        if (npx * ctx->rec_cap > ctx->rec_cap_px) {
+            cudaFree(ctx->rec);
+            cudaFree(ctx->rec_n);
+            ctx->rec = nullptr;
+            ctx->rec_n = nullptr;
+            ctx->rec_cap_px = 0;
+            CU(cudaMalloc(&ctx->rec, npx * ctx->rec_cap * sizeof(float2)));
+            CU(cudaMalloc(&ctx->rec_n, npx * sizeof(uint32_t) + 16));
+            ctx->rec_cap_px = npx * ctx->rec_cap;
+        }
+        CU(cudaMemsetAsync(ctx->rec_n, 0, npx * sizeof(uint32_t), ps));
+        ra.rec = ctx->rec;
+        ra.rec_n = ctx->rec_n;
+        ra.rec_cap = ctx->rec_cap;
+    }
     mark(10, ps);
     launch_raster(vp, ra, ctx->cfg.window_k, ps);
     mark(7, ps);
@@ -418,6 +446,11 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
     const size_t plane = (size_t)out_h * W;
     const bool dev_rgb = is_device_ptr(rgb);
     const bool dev_T = T ? is_device_ptr(T) : true;
+    const bool save = (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) != 0;
+    if (save && (n_views != 1 || row_begin != 0 || row_end != ty ||
+                 (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))))
+        return fail(ctx, AAA_ERR_INVALID_ARG, "AAA_FLAG_SAVE_CONTRIBS needs a single full-image default render");
+    ctx->saved = false;
     aaa_status s = enter(ctx);
     if (s) return s;
     for (int v = 0; v < n_views && !s; v++) {
@@ -428,9 +461,25 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
         float* ht = T && !dev_T ? T + plane * v : nullptr;
         s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0);
     }
+    if (save && !s) {
+        // a pixel that blended more than rec_cap contributions: grow the record and render again
+        const size_t npx = (size_t)W * H;
+        uint32_t* d_max = ctx->rec_n + npx;  // spare word after the counts
+        CU(cudaMemsetAsync(d_max, 0, sizeof(uint32_t), ctx->pstream));
+        launch_max_u32(ctx->rec_n, npx, d_max, ctx->pstream);
+        uint32_t mx = 0;
+        CU(cudaMemcpyAsync(&mx, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->pstream));
+        CU(cudaStreamSynchronize(ctx->pstream));
+        if (mx > ctx->rec_cap) {
+            while (ctx->rec_cap < mx) ctx->rec_cap *= 2;
+            s = run_view(ctx, cams[0], row_begin, row_end, dev_rgb ? rgb : nullptr, T && dev_T ? T : nullptr,
+                         dev_rgb ? nullptr : rgb, T && !dev_T ? T : nullptr, false, 0);
+        }
+    }
     aaa_status s2 = leave(ctx);
     if (s) return s;
     if (s2) return s2;
+    ctx->saved = save;
     if (!dev_rgb || !dev_T) return sync_all(ctx);
     return AAA_OK;
 }
@@ -441,6 +490,7 @@ aaa_status run_debug_view(aaa_ctx* ctx, bool debug_k1) {
     aaa_status s = enter(ctx);
     if (s) return s;
     ctx->cur ^= 1;
+    ctx->saved = false;
     s = run_view(ctx, ctx->cam, 0, ty, nullptr, nullptr, nullptr, nullptr, debug_k1, 1);
     aaa_status s2 = leave(ctx);
     if (s) return s;
@@ -490,6 +540,7 @@ void aaa_destroy(aaa_ctx* ctx) {
     SceneDev& s = ctx->scene;
     cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
     for (auto& sl : ctx->slot) free_slot(sl);
+    cudaFree(ctx->rec); cudaFree(ctx->rec_n); cudaFree(ctx->bwd_acc); cudaFree(ctx->bwd_overflow);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev_pool)
         for (auto x : e) cudaEventDestroy(x);
@@ -547,6 +598,7 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
     cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
     s = SceneDev{};
     ctx->loaded = false;
+    ctx->saved = false;
     const int64_t n = g->n;
     const int nf = 3 * (g->sh_degree + 1) * (g->sh_degree + 1);
     s.n = n;
@@ -686,6 +738,43 @@ aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_ca
     CU(cudaStreamSynchronize(st));
     if (out && !dev_out) cudaFree(d_out);
     cudaFree(d_cams);
+    return AAA_OK;
+}
+
+aaa_status aaa_render_backward(aaa_ctx* ctx, const float* dL_drgb, const float* dL_dT, float* d_means,
+                               float* d_scales, float* d_quats, float* d_opac, float* d_sh) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!ctx->saved) return fail(ctx, AAA_ERR_STATE, "no render saved with AAA_FLAG_SAVE_CONTRIBS");
+    if (!dL_drgb || !d_means || !d_scales || !d_quats || !d_opac || !d_sh)
+        return fail(ctx, AAA_ERR_INVALID_ARG, "null pointer");
+    const Slot& sl = ctx->slot[ctx->cur];
+    const int64_t n = ctx->scene.n;
+    CU(grow(ctx->bwd_acc, ctx->bwd_acc_cap, (size_t)(n > 0 ? n : 1) * BWD_ACC));
+    if (!ctx->bwd_overflow) CU(cudaMalloc(&ctx->bwd_overflow, sizeof(uint32_t)));
+    aaa_status s = enter(ctx);
+    if (s) return s;
+    cudaStream_t ps = ctx->pstream;
+    CU(cudaMemsetAsync(ctx->bwd_overflow, 0, sizeof(uint32_t), ps));
+    BwdArgs ba{};
+    ba.rec = ctx->rec;
+    ba.rec_n = ctx->rec_n;
+    ba.rec_cap = ctx->rec_cap;
+    ba.dL_drgb = dL_drgb;
+    ba.dL_dT = dL_dT;
+    ba.raster = sl.vb.raster;
+    ba.color = sl.vb.color;
+    ba.acc = ctx->bwd_acc;
+    ba.overflow = ctx->bwd_overflow;
+    ba.d_means = d_means; ba.d_scales = d_scales; ba.d_quats = d_quats; ba.d_opac = d_opac; ba.d_sh = d_sh;
+    launch_backward(ctx->scene, sl.vp, ba, ps);
+    CU(cudaGetLastError());
+    s = leave(ctx);
+    if (s) return s;
+    s = sync_all(ctx);
+    if (s) return s;
+    uint32_t ov = 0;
+    CU(cudaMemcpy(&ov, ctx->bwd_overflow, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (ov) return fail(ctx, AAA_ERR_STATE, std::to_string(ov) + " pixels blended more than 256 contributions");
     return AAA_OK;
 }
 

@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     rr[3] = make_float4((float)E2[2], (float)wref[0], (float)wref[1], (float)wref[2]);
     rr[4] = make_float4((float)wa[0], (float)wa[1], (float)wa[2], (float)wb[0]);
     rr[5] = make_float4((float)wb[1], (float)wb[2], (float)dot3(c, wref), (float)dot3(c, wa));
-    rr[6] = make_float4((float)dot3(c, wb), 0.f, 0.f, 0.f);
+    rr[6] = make_float4((float)dot3(c, wb), (float)c[0], (float)c[1], (float)c[2]);  // c: backward only
     vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
 
     uint32_t cnt = (ty0 <= ty1) ? (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1) : 0u;
