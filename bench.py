@@ -223,11 +223,19 @@ def run_ours(args, world, rank, local):
     from paper_2504_12811_b200 import _build
 
     _build.build()
+    # one process per GPU; with fewer GPUs than ranks (a functional test of the N > 1 path on one
+    # device), ranks share devices round-robin and AAA_DIST_BACKEND=gloo avoids NCCL's one-rank-
+    # per-GPU rule
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("AAA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2504_12811_b200 import partition as part
 
     # rank 0 builds the scene; NCCL broadcasts it (the only pre-render collective)
