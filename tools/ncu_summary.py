@@ -46,7 +46,7 @@ FULL_METRICS = [
 def base(name):
     n = re.sub(r"\(.*", "", name).replace("void ", "").strip()
     n = re.sub(r"^aaa::", "", n)
-    return re.sub(r"<.*", "", n) if n.startswith("k_raster<") else n
+    return re.sub(r"<.*", "", n)
 
 
 def main():
