@@ -80,13 +80,17 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         return lo;
     };
     int64_t g = find(cbeg, g0);
-    // the Gaussian's cull record, held in registers while consecutive candidates share it
-    // (eight 16-byte loads instead of a dependent load per field use)
-    union {
-        float4 v[sizeof(CullRec) / 16];
-        CullRec c;
-    } rr;
+    // per Gaussian, held in registers while consecutive candidates share it: the FP32 image of
+    // the quadratic and the record's small fields (the FP64 coefficients are re-read from global
+    // memory only by the rare guard-band re-test)
+    struct Hot {
+        float pref_x, pref_y;
+        uint16_t tx0, ty0, tx1, ty1, i0, j0, i1, j1;
+        int32_t cross_slot;
+        uint32_t zkey;
+    } r;
     int64_t g_loaded = -1;
+    QuadF qf{};
     uint32_t keep_mask = 0, nkeep = 0;
     const bool no_cull = (vp.flags & AAA_FLAG_NO_TILE_CULL) != 0;
 #pragma unroll 1
@@ -95,25 +99,43 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         if (c >= C) break;
         if (g < g1 && off(g + 1) <= c) g = find(c, g + 1);  // next Gaussian (skips empty runs)
         if (g != g_loaded) {
+            union {
+                float4 v[sizeof(CullRec) / 16];
+                CullRec c;
+            } rr;
             const float4* src = reinterpret_cast<const float4*>(cull + g);
 #pragma unroll
             for (int q = 0; q < (int)(sizeof(CullRec) / 16); q++) rr.v[q] = __ldg(&src[q]);
             g_loaded = g;
+            const CullRec& r0 = rr.c;
+            qf = QuadF{(float)r0.qa, (float)r0.qb, (float)r0.qc, (float)r0.qd, (float)r0.qe, (float)r0.qf,
+                       (float)r0.ia, (float)r0.ic, (float)r0.xs, (float)r0.ys, (float)r0.qi};
+            r = Hot{r0.pref_x, r0.pref_y, r0.tx0, r0.ty0, r0.tx1, r0.ty1, r0.i0, r0.j0, r0.i1, r0.j1,
+                    r0.cross_slot, r0.zkey};
         }
-        const CullRec& r = rr.c;
         uint32_t j = c - off(g);
         uint32_t w = (uint32_t)r.tx1 - r.tx0 + 1;
         int tx = r.tx0 + (int)(j % w), ty = r.ty0 + (int)(j / w);
-        double x0 = TILE * tx + 0.5, x1 = fmin(TILE * tx + TILE - 0.5, vp.width - 0.5);
-        double y0 = TILE * ty + 0.5, y1 = fmin(TILE * ty + TILE - 0.5, vp.height - 0.5);
+        // pixel-centre box of the tile (exact in FP32: k + 0.5 with k < 2^23)
+        const float x0 = TILE * tx + 0.5f, x1 = fminf(TILE * tx + TILE - 0.5f, vp.width - 0.5f);
+        const float y0 = TILE * ty + 0.5f, y1 = fminf(TILE * ty + TILE - 0.5f, vp.height - 0.5f);
         bool keep;
         uint32_t sub = SUBTILE_ALL;
         if (no_cull) {
             keep = true;
         } else if (r.cross_slot < 0) {
-            double px = r.pref_x, py = r.pref_y;
-            keep = quad_box_min_pre(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, r.ia, r.ic, r.xs, r.ys, r.qi, x0 - px,
-                                    x1 - px, y0 - py, y1 - py) < 0.0;
+            // exact sign of the FP64 box minimum: FP32 outside the guard band, FP64 inside it
+            auto box_keep = [&](float bx0, float bx1, float by0, float by1) -> bool {
+#ifndef AAA_K3_F64ONLY
+                const int sg = quad_box_sign_f32(qf, bx0 - r.pref_x, bx1 - r.pref_x, by0 - r.pref_y, by1 - r.pref_y);
+                if (sg >= 0) return sg == 1;
+#endif
+                const CullRec& rd = cull[g];
+                const double px = r.pref_x, py = r.pref_y;
+                return quad_box_min_pre(rd.qa, rd.qb, rd.qc, rd.qd, rd.qe, rd.qf, rd.ia, rd.ic, rd.xs, rd.ys, rd.qi,
+                                        (double)bx0 - px, (double)bx1 - px, (double)by0 - py, (double)by1 - py) < 0.0;
+            };
+            keep = box_keep(x0, x1, y0, y1);
             if (keep) {
                 // the same exact test on each 8x4 warp sub-tile (pixel-centre rects): the raster
                 // kernels skip the Gaussian on sub-tiles whose bit is clear ("repeated culling")
@@ -123,12 +145,10 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
                     const int spx = TILE * tx + 8 * (s & 1), spy = TILE * ty + 4 * (s >> 1);
                     // sub-tiles outside the Gaussian's pixel rect hold no contributing pixel (bounds)
                     if (spx > r.i1 || spx + 7 < r.i0 || spy > r.j1 || spy + 3 < r.j0) continue;
-                    double sx0 = spx + 0.5, sy0 = spy + 0.5;
-                    if (sx0 > vp.width - 0.5 || sy0 > vp.height - 0.5) continue;
-                    double sx1 = fmin(sx0 + 7.0, vp.width - 0.5), sy1 = fmin(sy0 + 3.0, vp.height - 0.5);
-                    if (quad_box_min_pre(r.qa, r.qb, r.qc, r.qd, r.qe, r.qf, r.ia, r.ic, r.xs, r.ys, r.qi,
-                                         sx0 - px, sx1 - px, sy0 - py, sy1 - py) < 0.0)
-                        sub |= 1u << s;
+                    const float sx0 = spx + 0.5f, sy0 = spy + 0.5f;
+                    if (sx0 > vp.width - 0.5f || sy0 > vp.height - 0.5f) continue;
+                    const float sx1 = fminf(sx0 + 7.f, vp.width - 0.5f), sy1 = fminf(sy0 + 3.f, vp.height - 0.5f);
+                    if (box_keep(sx0, sx1, sy0, sy1)) sub |= 1u << s;
                 }
             }
         } else {

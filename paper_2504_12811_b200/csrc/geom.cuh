@@ -77,6 +77,46 @@ __device__ __forceinline__ double quad_box_min_pre(double a, double b, double c,
     return m;
 }
 
+// FP32 image of quad_box_min_pre's coefficients (K3's fast path).
+struct QuadF {
+    float a, b, c, d, e, f, ia, ic, xs, ys, qi;
+};
+
+// Sign of quad_box_min_pre decided in FP32 with a guard band, FP64 only inside the band.
+// Every FP32 candidate value differs from its FP64 counterpart by at most ~8 * 2^-24 * S, where
+// S = |a|X^2 + 2|b|XY + 2|d|X + |c|Y^2 + 2|e|Y + |f| (X, Y the box's largest |x|, |y|): one
+// rounding per coefficient, per coordinate and per FMA of the Horner form, each bounded by the
+// magnitude of the terms; an edge critical point computed in FP32 moves q by O(c dy^2), second
+// order. With the band at 2^-17 S (16x that bound) a decision outside the band is the FP64
+// decision, so the kept set is bit-identical to the all-FP64 test.
+// Returns 1 (q < 0 somewhere: keep), 0 (reject), -1 (inside the band: re-test in FP64).
+__device__ __forceinline__ int quad_box_sign_f32(const QuadF& Q, float x0, float x1, float y0, float y1) {
+    auto q = [&](float x, float y) {
+        return fmaf(fmaf(Q.a, x, fmaf(2.f * Q.b, y, 2.f * Q.d)), x, fmaf(fmaf(Q.c, y, 2.f * Q.e), y, Q.f));
+    };
+    float m = fminf(fminf(q(x0, y0), q(x1, y0)), fminf(q(x0, y1), q(x1, y1)));
+    if (Q.ic > 0.f) {
+        const float ya = -fmaf(Q.b, x0, Q.e) * Q.ic, yb = -fmaf(Q.b, x1, Q.e) * Q.ic;
+        if (ya > y0 && ya < y1) m = fminf(m, q(x0, ya));
+        if (yb > y0 && yb < y1) m = fminf(m, q(x1, yb));
+    }
+    if (Q.ia > 0.f) {
+        const float xa = -fmaf(Q.b, y0, Q.d) * Q.ia, xb = -fmaf(Q.b, y1, Q.d) * Q.ia;
+        if (xa > x0 && xa < x1) m = fminf(m, q(xa, y0));
+        if (xb > x0 && xb < x1) m = fminf(m, q(xb, y1));
+    }
+    if (Q.xs >= x0 && Q.xs <= x1 && Q.ys >= y0 && Q.ys <= y1) m = fminf(m, Q.qi);
+    const float X = fmaxf(fabsf(x0), fabsf(x1)), Y = fmaxf(fabsf(y0), fabsf(y1));
+    const float S = fmaf(fmaf(fabsf(Q.a), X, 2.f * fmaf(fabsf(Q.b), Y, fabsf(Q.d))), X,
+                         fmaf(fmaf(fabsf(Q.c), Y, 2.f * fabsf(Q.e)), Y, fabsf(Q.f)));
+    // a non-finite or tiny scale (FP32 underflow of the coefficients) always takes the FP64 test
+    if (!(S > 1e-30f && S < 1e30f)) return -1;
+    const float band = S * 0x1p-17f;
+    if (m < -band) return 1;
+    if (m > band) return 0;
+    return -1;
+}
+
 // Exact minimum of rho^2 = |u|^2 over the frustum {pixel-centre rect [x0,x1]x[y0,y1]} ∩
 // {z >= near} (readings 20-21). The five view-space half-spaces n.x + d >= 0 are
 // pulled back to Gaussian space through x = M u + mu_v (Eq. 5); the convex QP is solved by
