@@ -800,8 +800,9 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
 #ifdef AAA_DEBUG_STATS
     {
         const unsigned long long* u = reinterpret_cast<const unsigned long long*>(&h[20]);
-        fprintf(stderr, "[aaa debug] inserts=%llu shifts=%llu far_shifts=%llu sum_cnt=%llu ins_cnt16=%llu k6s_max_pending=%u\n",
-                u[0], u[1], u[2], u[3], u[4], h[30]);
+        fprintf(stderr, "[aaa debug] inserts=%llu shifts=%llu far_shifts=%llu sum_cnt=%llu ins_cnt16=%llu k6s_max_pending=%u"
+                " k6s_rounds=%u k6s_matched=%u k6s_max_rounds=%u\n",
+                u[0], u[1], u[2], u[3], u[4], h[30], h[18], h[19], h[31]);
     }
 #endif
     out->launches = ctx->launches;

@@ -271,12 +271,14 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 #ifndef AAA_K1_MINB
 #define AAA_K1_MINB 3  // 168 registers: 3 CTAs of 128 threads per SM (A/B: 0.78 -> 0.69 ms on c3)
 #endif
-__global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, ViewParams vp, ViewBufs vb, int debug) {
+// DBG: the parity-test instantiation that also writes the per-Gaussian debug fields
+template <bool DBG>
+__global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, ViewParams vp, ViewBufs vb) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= sc.n) return;
     const double INF = CUDART_INF;
     float4 A4 = __ldg(&sc.geomA[g]), B4 = __ldg(&sc.geomB[g]), C4 = __ldg(&sc.geomC[g]);
-    double* dbg = debug ? vb.dbg + g * AAA_DBG_GAUSS_FIELDS : nullptr;
+    double* dbg = DBG ? vb.dbg + g * AAA_DBG_GAUSS_FIELDS : nullptr;
     if (dbg)
         for (int i = 0; i < AAA_DBG_GAUSS_FIELDS; i++) dbg[i] = 0.0;
     vb.counts[g] = 0;
@@ -450,10 +452,6 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
         zkey = (uint32_t)fmin(fmax(floor(um), 0.0), qmax);
     }
 
-    // --- colour (reading 15): SH at d = (mu - o)/|mu - o|
-    float rgb[3];
-    sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
-
     int slot = -1;
     if (crossing) {
         slot = (int)atomicAdd(&vb.counters[CNT_CROSS], 1u);
@@ -495,6 +493,11 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     rr[4] = make_float4((float)wa[0], (float)wa[1], (float)wa[2], (float)wb[0]);
     rr[5] = make_float4((float)wb[1], (float)wb[2], (float)dot3(c, wref), (float)dot3(c, wa));
     rr[6] = make_float4((float)dot3(c, wb), (float)c[0], (float)c[1], (float)c[2]);  // c: backward only
+
+    // --- colour (reading 15): SH at d = (mu - o)/|mu - o| (after the record writes, so the FP64
+    // geometry is dead while the 48 SH coefficients are live: fewer registers, more resident warps)
+    float rgb[3];
+    sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
     vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
 
     uint32_t cnt = (ty0 <= ty1) ? (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1) : 0u;
@@ -518,8 +521,10 @@ void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, b
     unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
     if (vp.flags & AAA_FLAG_NO_3D)
         k_preprocess_2d<<<blocks, threads, 0, st>>>(sc, vp, vb);
+    else if (debug)
+        k_preprocess<true><<<blocks, threads, 0, st>>>(sc, vp, vb);
     else
-        k_preprocess<<<blocks, threads, 0, st>>>(sc, vp, vb, debug ? 1 : 0);
+        k_preprocess<false><<<blocks, threads, 0, st>>>(sc, vp, vb);
 }
 
 }  // namespace aaa
