@@ -91,11 +91,13 @@ typedef struct {
  * since the previous aaa_get_stats call (timed_views of them; the accumulation is reset by
  * the call): 0 preprocess (K1), 1 scan (K2), 2 cull/emit (K3), 3 sort (K4), 4 ranges (K5),
  * 5 raster (K6), 6 spilled-pixel continuation (K6s), 7 host-sync gap after K2, 8 output copy
- * (host outputs only), 9 total. */
+ * (host outputs only), 9 total. deep_pixels: spilled pixels whose pending set outgrew K6s's
+ * 256 entries (finished by K6d with 2048). */
 typedef struct {
     int64_t n, visible, candidates, pairs, spilled_pixels, unresolved_pixels, crossing;
     int64_t evaluations, launches, timed_views;
     float ms[10];
+    int64_t deep_pixels;
 } aaa_stats;
 
 /* aaa_config.flags:
@@ -104,6 +106,8 @@ typedef struct {
  *                            (no 3D tile test, no sub-tile masks); the image is unchanged
  *   AAA_FLAG_FORCE_FALLBACK  window K = 1: every pixel with two pending entries continues in the
  *                            spill kernel (test of the exact continuation; the image is unchanged)
+ *   AAA_FLAG_FORCE_DEEP      K6s hands every pixel whose pending set exceeds 32 entries to K6d
+ *                            (test of the second spill level; the image is unchanged)
  *   AAA_FLAG_NO_HIER_SORT    Table 5 "w/o hier. sort": blend in the global per-Gaussian
  *                            order only — tile lists sorted by the view depth of the mean, no
  *                            per-pixel re-sort (the image changes where that order is not z*)
@@ -122,6 +126,7 @@ enum {
     AAA_FLAG_SAVE_CONTRIBS = 32u  /* aaa_render records each pixel's blended contributions (in blend
                                    * order) for aaa_render_backward; single full-image default renders
                                    * only; the call synchronises */
+    , AAA_FLAG_FORCE_DEEP = 64u
 };
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */

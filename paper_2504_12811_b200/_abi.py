@@ -8,6 +8,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libaaa.so"
 
 AAA_FLAG_TIMING, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_FORCE_FALLBACK, AAA_FLAG_NO_HIER_SORT, AAA_FLAG_NO_3D = 1, 2, 4, 8, 16
 AAA_FLAG_SAVE_CONTRIBS = 32
+AAA_FLAG_FORCE_DEEP = 64
 (AAA_DBG_GAUSS, AAA_DBG_KEYS, AAA_DBG_VALS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_VALS_UNSORTED, AAA_DBG_RANGES,
  AAA_DBG_SPILL, AAA_DBG_RASTER, AAA_DBG_COLOR) = range(9)
 AAA_DBG_GAUSS_FIELDS = 26
@@ -46,7 +47,8 @@ class Gaussians(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("n", C.c_int64), ("visible", C.c_int64), ("candidates", C.c_int64), ("pairs", C.c_int64),
                 ("spilled_pixels", C.c_int64), ("unresolved_pixels", C.c_int64), ("crossing", C.c_int64), ("evaluations", C.c_int64),
-                ("launches", C.c_int64), ("timed_views", C.c_int64), ("ms", C.c_float * 10)]
+                ("launches", C.c_int64), ("timed_views", C.c_int64), ("ms", C.c_float * 10),
+                ("deep_pixels", C.c_int64)]
 
 
 _lib = None

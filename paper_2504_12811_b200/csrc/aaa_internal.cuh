@@ -96,9 +96,14 @@ struct ViewBufs {
     uint32_t* scan_state; // decoupled look-back state for the scan / emit / sort
 };
 
+// K6s pending-set capacity per pixel (first spill level; the deep level K6d holds 2048)
+#ifndef AAA_SP_CAP
+#define AAA_SP_CAP 256
+#endif
+constexpr int AAA_SP_CAP_LVL1 = AAA_SP_CAP;
 constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_SPILL = 4, CNT_SPILL_TICKET = 5,
               CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
-              CNT_TOTAL = 32;
+              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_TOTAL = 40;
 
 // ---- launchers (each file implements its own) ----
 void launch_load_pack(const aaa_gaussians& in, const float* dmeans, const float* dscales, const float* dquats,
@@ -144,6 +149,10 @@ struct RasterArgs {
     float4* spill_e;      // spill_k window entries per spilled pixel: (z, alpha, g bits, 0)
     uint32_t spill_cap;
     uint32_t spill_k;
+    SpillHdr* deep_hdr;   // pixels whose K6s pending set overflowed (K6s -> K6d)
+    float4* deep_e;       // deep_k entries per deep pixel: (z, alpha, g bits, order bits)
+    uint32_t deep_cap;    // slots
+    uint32_t deep_k;      // >= the K6s pending limit
     uint32_t* counters;
     // backward support (AAA_FLAG_SAVE_CONTRIBS): every blended contribution of pixel p, in blend
     // order, as (g bits, alpha) at rec[p * rec_cap + i]; rec_n[p] = count (may exceed rec_cap:

@@ -37,6 +37,10 @@ struct Slot {
     float4* spill_e = nullptr;
     size_t spill_cap = 0;
     int spill_k = 0;
+    SpillHdr* deep_hdr = nullptr;  // K6s -> K6d queue
+    float4* deep_e = nullptr;
+    size_t deep_slots = 0;
+    int deep_k = 0;
     float* d_out = nullptr;  // staging image for host outputs
     size_t d_out_cap = 0;
     cudaEvent_t prep_done = nullptr, raster_done = nullptr;
@@ -187,7 +191,8 @@ void free_slot(Slot& s) {
     cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
     for (int i = 0; i < 2; i++) { cudaFree(s.sb.keys[i]); cudaFree(s.sb.vals[i]); }
     cudaFree(s.sb.hist); cudaFree(s.sb.state); cudaFree(s.sb.tickets);
-    cudaFree(s.ranges); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.d_out);
+    cudaFree(s.ranges); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
+    cudaFree(s.d_out);
     if (s.prep_done) cudaEventDestroy(s.prep_done);
     if (s.raster_done) cudaEventDestroy(s.raster_done);
     s = Slot{};
@@ -226,6 +231,26 @@ aaa_status ensure_tiles(aaa_ctx* ctx, Slot& sl, int n_tiles) {
 // Spill slots for pixels whose K6 window fills: one per pixel up to 4M per view (beyond that a
 // pixel is counted as unresolved by aaa_get_stats), each holding the window's K entries.
 constexpr size_t MAX_SPILL = (size_t)1 << 22;
+// Deep queue: pixels whose K6s pending set outgrows its AAA_SP_CAP_LVL1 entries (none on c1-c5 so
+// far; beyond the queue's slots a pixel is counted as unresolved). AAA_FLAG_FORCE_DEEP (K6s limit
+// 32) uses a wider, shallower queue.
+constexpr size_t DEEP_SLOTS = 4096, DEEP_SLOTS_FORCED = (size_t)1 << 18;
+
+aaa_status ensure_deep(aaa_ctx* ctx, Slot& sl, bool forced) {
+    const size_t slots = forced ? DEEP_SLOTS_FORCED : DEEP_SLOTS;
+    const int k = forced ? 32 : AAA_SP_CAP_LVL1;
+    if (sl.deep_hdr && sl.deep_slots == slots && sl.deep_k == k) return AAA_OK;
+    cudaFree(sl.deep_hdr);
+    cudaFree(sl.deep_e);
+    sl.deep_hdr = nullptr;
+    sl.deep_e = nullptr;
+    sl.deep_slots = 0;
+    CU(cudaMalloc(&sl.deep_hdr, slots * sizeof(SpillHdr)));
+    CU(cudaMalloc(&sl.deep_e, slots * (size_t)k * sizeof(float4)));
+    sl.deep_slots = slots;
+    sl.deep_k = k;
+    return AAA_OK;
+}
 
 aaa_status ensure_spill(aaa_ctx* ctx, Slot& sl, size_t pixels, int k) {
     size_t cap = std::min(pixels, MAX_SPILL);
@@ -362,6 +387,12 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.spill_e = sl.spill_e;
     ra.spill_cap = (uint32_t)sl.spill_cap;
     ra.spill_k = (uint32_t)sl.spill_k;
+    s = ensure_deep(ctx, sl, (ctx->cfg.flags & AAA_FLAG_FORCE_DEEP) != 0);
+    if (s) return s;
+    ra.deep_hdr = sl.deep_hdr;
+    ra.deep_e = sl.deep_e;
+    ra.deep_cap = (uint32_t)sl.deep_slots;
+    ra.deep_k = (uint32_t)sl.deep_k;
     ra.counters = sl.vb.counters;
     if (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) {
         const size_t npx = (size_t)cam.width * cam.height;
@@ -796,6 +827,7 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     out->spilled_pixels = h[CNT_SPILL];
     out->unresolved_pixels = h[CNT_UNRESOLVED];
     out->crossing = h[CNT_CROSS];
+    out->deep_pixels = h[CNT_DEEP];
     out->evaluations = h[CNT_EVAL];
 #ifdef AAA_DEBUG_STATS
     {

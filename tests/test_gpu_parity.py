@@ -250,10 +250,16 @@ def test_determinism_and_window_independence(R):
     R.set_config(window_k=32, flags=pkg.AAA_FLAG_FORCE_FALLBACK)
     d = _img(R, cam)
     st = R.stats()
+    # second spill level: K6s hands every pending set above 32 entries to K6d
+    R.set_config(window_k=32, flags=pkg.AAA_FLAG_FORCE_FALLBACK | pkg.AAA_FLAG_FORCE_DEEP)
+    e = _img(R, cam)
+    st_deep = R.stats()
     R.set_config(window_k=32, flags=0)
     assert np.array_equal(a, c)
     assert np.array_equal(a, d), np.abs(a - d).max()
     assert st["spilled_pixels"] > 10000 and st["unresolved_pixels"] == 0, st
+    assert np.array_equal(a, e), np.abs(a - e).max()
+    assert st_deep["deep_pixels"] > 100 and st_deep["unresolved_pixels"] == 0, st_deep
 
 
 def test_empty_scene_and_all_culled(R):
