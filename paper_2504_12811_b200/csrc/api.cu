@@ -416,7 +416,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     mark(7, ps);
     launch_raster_fallback(vp, ra, ps);
     mark(8, ps);
-    if (vp.tile_row_end > vp.tile_row_begin) ctx->launches += 3;
+    if (vp.tile_row_end > vp.tile_row_begin) ctx->launches += 3;  // K6, K6s, K6d
     if (host_rgb || host_T) {
         // image D2H on the copy stream, overlapping the next view's kernels
         CU(cudaEventRecord(sl.prep_done, ps));
