@@ -83,7 +83,7 @@ def main():
         d = dict(zip(hh, x))
         kern.append((base(d["Kernel Name"]), d))
     lines = [f"# {r}: ncu --set full of one c3 view (every kernel, 2nd rendered view)", "",
-             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 13 -c 12 "
+             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 14 -c 13 "
              "python bench.py --steps 1 --warmup 3 --views-per-rank 1 --no-cpu-baseline --no-e2e`. "
              "ncu flushes caches before each replay (cold L2).", "",
              "| metric | " + " | ".join(k for k, _ in kern) + " |", "|---|" + "---|" * len(kern)]
