@@ -15,7 +15,13 @@
 
 namespace aaa {
 
-constexpr int SORT_THREADS = 256, SORT_ITEMS = 16, SORT_TILE = SORT_THREADS * SORT_ITEMS, SORT_WARPS = 8;
+#ifndef AAA_SORT_ITEMS
+#define AAA_SORT_ITEMS 16
+#endif
+#ifndef AAA_SORT_MINB
+#define AAA_SORT_MINB 3  // 80 registers, 3 CTAs per SM (A/B on c3: 1 -> 0.25-0.35 ms, 3 -> 0.215 ms)
+#endif
+constexpr int SORT_THREADS = 256, SORT_ITEMS = AAA_SORT_ITEMS, SORT_TILE = SORT_THREADS * SORT_ITEMS, SORT_WARPS = 8;
 constexpr int MAX_PASSES = 8;
 
 int sort_passes(int key_bits) { return (key_bits + 7) / 8; }
@@ -49,7 +55,7 @@ __global__ void k_sort_hist_scan(uint32_t* hist) {
     h[threadIdx.x] = e;
 }
 
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const skey_t* __restrict__ kin,
+__global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const skey_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin,
                                                            skey_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            const uint32_t* d_count, int shift,
