@@ -368,12 +368,14 @@ def run_ours(args, world, rank, local):
         res = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-               "data": "synthetic (seeded c3 generator; no datasets or trained weights exist offline)",
-               "config": {"workload": f"{args.config}: 3M Gaussians SH3, 1920x1080, 200-view orbit; "
-                                      f"{len(views)} views per rank per step",
+               "data": f"synthetic (seeded {args.config} generator; no datasets or trained weights exist offline)",
+               "config": {"workload": f"{args.config}: {n / 1e6:g}M Gaussians SH{sh_deg}, {W}x{H}, "
+                                      f"{len(cams)}-view set; {len(views)} views per rank per step",
                           "views_per_rank_per_step": len(views), "ablation": args.ablation, "gaussians": n, "width": W, "height": H,
-                          "parallelism": f"view-sharded x{world}", "l2": "inputs larger than L2 (720 MB scene "
-                          "re-streamed per view), no flush"},
+                          "parallelism": f"view-sharded x{world}",
+                          "l2": (f"inputs larger than L2 ({n * 240 / 1e6:.0f} MB scene re-streamed per view), no flush"
+                                 if n * 240 > 126e6 else
+                                 f"scene ({n * 240 / 1e6:.0f} MB) fits in L2 and stays resident across views, no flush")},
                "mpix_per_s": value * W * H / 1e6,
                "roofline": roof, "stages": stages, "counters_per_view": mean,
                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
