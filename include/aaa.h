@@ -108,6 +108,8 @@ typedef struct {
  *                            spill kernel (test of the exact continuation; the image is unchanged)
  *   AAA_FLAG_FORCE_DEEP      K6s hands every pixel whose pending set exceeds 32 entries to K6d
  *                            (test of the second spill level; the image is unchanged)
+ *   AAA_FLAG_CULL_FP64       K3 decides every tile / sub-tile test in FP64 (no FP32 guard-band
+ *                            fast path; test of the guard band: the pairs are unchanged)
  *   AAA_FLAG_NO_HIER_SORT    Table 5 "w/o hier. sort": blend in the global per-Gaussian
  *                            order only — tile lists sorted by the view depth of the mean, no
  *                            per-pixel re-sort (the image changes where that order is not z*)
@@ -127,6 +129,7 @@ enum {
                                    * order) for aaa_render_backward; single full-image default renders
                                    * only; the call synchronises */
     , AAA_FLAG_FORCE_DEEP = 64u
+    , AAA_FLAG_CULL_FP64 = 128u
 };
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */

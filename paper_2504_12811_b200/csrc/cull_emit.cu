@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     QuadF qf{};
     uint32_t keep_mask = 0, nkeep = 0;
     const bool no_cull = (vp.flags & AAA_FLAG_NO_TILE_CULL) != 0;
+    const bool f64_only = (vp.flags & AAA_FLAG_CULL_FP64) != 0;  // guard-band test switch
 #pragma unroll 1
     for (int k = 0; k < EMIT_ITEMS; k++) {
         uint32_t c = cbeg + k;
@@ -126,10 +127,10 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         } else if (r.cross_slot < 0) {
             // exact sign of the FP64 box minimum: FP32 outside the guard band, FP64 inside it
             auto box_keep = [&](float bx0, float bx1, float by0, float by1) -> bool {
-#ifndef AAA_K3_F64ONLY
-                const int sg = quad_box_sign_f32(qf, bx0 - r.pref_x, bx1 - r.pref_x, by0 - r.pref_y, by1 - r.pref_y);
-                if (sg >= 0) return sg == 1;
-#endif
+                if (!f64_only) {
+                    const int sg = quad_box_sign_f32(qf, bx0 - r.pref_x, bx1 - r.pref_x, by0 - r.pref_y, by1 - r.pref_y);
+                    if (sg >= 0) return sg == 1;
+                }
                 const CullRec& rd = cull[g];
                 const double px = r.pref_x, py = r.pref_y;
                 return quad_box_min_pre(rd.qa, rd.qb, rd.qc, rd.qd, rd.qe, rd.qf, rd.ia, rd.ic, rd.xs, rd.ys, rd.qi,

@@ -199,6 +199,23 @@ def test_sort_bit_exact_and_ranges(R, cfg):
         assert st["pairs"] == len(ks) and st["candidates"] >= st["pairs"] > 1_000_000
 
 
+@pytest.mark.parametrize("cfg,view", [("c2", 0), ("c3", 0), ("c4wide", 3), ("c4inside", 49)])
+def test_cull_fp32_guard_band_equals_fp64(R, cfg, view):
+    """K3's FP32 box-minimum sign with the 2^-17 S guard band (K3 guard band) keeps
+    exactly the pairs and 8x4 sub-tile masks of the all-FP64 test, in the same order."""
+    scene, cams = S.make_config(cfg)
+    cam = cams[view]
+    R.load(scene)
+    R.render(cam, with_T=False)
+    ku, vu = R.keys_vals(sorted_=False)
+    R.set_config(flags=pkg.AAA_FLAG_CULL_FP64)
+    R.render(cam, with_T=False)
+    ku64, vu64 = R.keys_vals(sorted_=False)
+    R.set_config(flags=0)
+    assert len(ku) > 1000
+    assert np.array_equal(ku, ku64) and np.array_equal(vu, vu64)
+
+
 # ------------------------------------------------------------------ images
 def test_image_c1_full(R):
     scene, cams = S.make_config("c1")
