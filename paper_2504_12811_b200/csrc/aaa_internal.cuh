@@ -139,6 +139,7 @@ struct RasterArgs {
     const skey_t* keys;
     const uint32_t* vals;
     const uint2* ranges;
+    uint32_t* tile_order;  // K6 launch order of the tiles (written by k_tile_order)
     const float4* raster;
     const float4* color;
     float* out_rgb;       // 3 x out_h x W

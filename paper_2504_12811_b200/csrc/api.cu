@@ -32,6 +32,7 @@ struct Slot {
     uint32_t pair_cap = 0;
     size_t sort_state_cap = 0;
     uint2* ranges = nullptr;
+    uint32_t* tile_order = nullptr;  // K6 tile launch order (longest list first)
     int ranges_cap = 0;
     SpillHdr* spill_hdr = nullptr;
     float4* spill_e = nullptr;
@@ -191,7 +192,7 @@ void free_slot(Slot& s) {
     cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
     for (int i = 0; i < 2; i++) { cudaFree(s.sb.keys[i]); cudaFree(s.sb.vals[i]); }
     cudaFree(s.sb.hist); cudaFree(s.sb.state); cudaFree(s.sb.tickets);
-    cudaFree(s.ranges); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
+    cudaFree(s.ranges); cudaFree(s.tile_order); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
     cudaFree(s.d_out);
     if (s.prep_done) cudaEventDestroy(s.prep_done);
     if (s.raster_done) cudaEventDestroy(s.raster_done);
@@ -222,8 +223,11 @@ aaa_status ensure_view_bufs(aaa_ctx* ctx, Slot& sl, int64_t n) {
 aaa_status ensure_tiles(aaa_ctx* ctx, Slot& sl, int n_tiles) {
     if (n_tiles <= sl.ranges_cap) return AAA_OK;
     cudaFree(sl.ranges);
+    cudaFree(sl.tile_order);
     sl.ranges = nullptr;
+    sl.tile_order = nullptr;
     CU(cudaMalloc(&sl.ranges, (size_t)n_tiles * sizeof(uint2)));
+    CU(cudaMalloc(&sl.tile_order, (size_t)n_tiles * sizeof(uint32_t)));
     sl.ranges_cap = n_tiles;
     return AAA_OK;
 }
@@ -370,6 +374,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.keys = sl.sb.keys[sorted];
     ra.vals = sl.sb.vals[sorted];
     ra.ranges = sl.ranges;
+    ra.tile_order = sl.tile_order;
     ra.raster = sl.vb.raster;
     ra.color = sl.vb.color;
     if (!rgb || (!T && host_T)) {
@@ -416,7 +421,8 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     mark(7, ps);
     launch_raster_fallback(vp, ra, ps);
     mark(8, ps);
-    if (vp.tile_row_end > vp.tile_row_begin) ctx->launches += 3;  // K6, K6s, K6d
+    if (vp.tile_row_end > vp.tile_row_begin)  // [tile order,] K6, K6s, K6d
+        ctx->launches += (ctx->cfg.flags & (AAA_FLAG_NO_3D | AAA_FLAG_NO_HIER_SORT)) ? 3 : 4;
     if (host_rgb || host_T) {
         // image D2H on the copy stream, overlapping the next view's kernels
         CU(cudaEventRecord(sl.prep_done, ps));

@@ -23,7 +23,7 @@ STAGE_KERNELS = {
     "cull_emit": ["k_cull_emit"],
     "sort": ["k_sort_hist", "k_sort_hist_scan", "k_onesweep"],
     "ranges": ["k_ranges"],
-    "raster": ["k_raster", "k_raster_spill"],
+    "raster": ["k_tile_order", "k_raster", "k_raster_spill"],
 }
 
 FULL_METRICS = [
@@ -83,7 +83,7 @@ def main():
         d = dict(zip(hh, x))
         kern.append((base(d["Kernel Name"]), d))
     lines = [f"# {r}: ncu --set full of one c3 view (every kernel, 2nd rendered view)", "",
-             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 14 -c 13 "
+             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 14 "
              "python bench.py --steps 1 --warmup 3 --views-per-rank 1 --no-cpu-baseline --no-e2e`. "
              "ncu flushes caches before each replay (cold L2).", "",
              "| metric | " + " | ".join(k for k, _ in kern) + " |", "|---|" + "---|" * len(kern)]

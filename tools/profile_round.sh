@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     python bench.py --steps 2 --warmup 3 --views-per-rank 4 --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/ncu_launch_${R}.err
 tail -3 gpurun_out/ncu_launch_${R}.err
 # full capture of one whole view (the 2nd rendered view: skip the load kernel + the first view)
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_ -s 14 -c 13 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 14 \
     -o gpurun_out/full_${R} -f \
     python bench.py --steps 1 --warmup 3 --views-per-rank 1 --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/ncu_full_${R}.err
 tail -3 gpurun_out/ncu_full_${R}.err
