@@ -56,6 +56,10 @@ struct SceneDev {
     float4* sh;      // SoA chunks: sh[c * n + g], c < 3*(deg+1)^2/4 (rounded up); floats in
                      // coefficient-major, channel-minor order
     int sh_chunks;
+    // internal -> caller index: the scene is stored in Morton order of the means (aaa_load_gaussians)
+    // so that warps and tile lists touch spatially coherent Gaussians; per-Gaussian outputs
+    // (gradients, v_train, debug records) are written back in the caller's order through it
+    uint32_t* perm;
 };
 
 // K3 input per visible Gaussian (128 B): screen-space quadratic q(p) = N(p) - tau Q(p) relative
@@ -127,6 +131,8 @@ int sort_passes(int key_bits);
 size_t sort_state_words(uint32_t cap, int passes);
 // returns the index (0/1) of the buffer holding the sorted output
 int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st);
+void launch_tie_fix(const skey_t* keys, uint32_t* vals, const uint32_t* d_count, uint32_t cap, const uint32_t* perm,
+                    cudaStream_t st);
 void launch_ranges(const skey_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles, int key_db,
                    cudaStream_t st);
 // exact state of a pixel whose K6 window filled: K6s resumes it at list position `pos`
@@ -187,6 +193,10 @@ struct VtCam {
     double R[9], t[3];
     double fx, fy, cx, cy, near_z, f, w, h;
 };
+void launch_morton_order(const SceneDev& sc, uint32_t* keys, uint32_t* vals, const float* lo_hi, cudaStream_t st);
+int aabb_blocks(int64_t n);
+void launch_aabb(const SceneDev& sc, float* d_blk, cudaStream_t st);
+void launch_permute(const float4* in, float4* out, const uint32_t* perm, int64_t n, int chunks, cudaStream_t st);
 void launch_vtrain(const SceneDev& sc, const VtCam* cams, int n_cams, float* out, bool store, cudaStream_t st);
 void launch_raster_fallback(const ViewParams& vp, const RasterArgs& ra, cudaStream_t st);
 

@@ -69,6 +69,7 @@ struct aaa_ctx {
     std::vector<std::vector<cudaEvent_t>> ev_pool;
     size_t ev_used = 0;
     int64_t launches = 0;
+    std::vector<uint32_t> h_perm;  // internal -> caller Gaussian index (host copy of scene.perm)
     // backward support (AAA_FLAG_SAVE_CONTRIBS): the last single-view render's blend records
     float2* rec = nullptr;
     size_t rec_cap_px = 0;  // pixels x entries the record buffer holds
@@ -364,6 +365,10 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     }
     int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_P], C, key_bits, ps);
     sl.sorted = sorted;
+    if (ctx->scene.perm && (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))) {
+        launch_tie_fix(sl.sb.keys[sorted], sl.sb.vals[sorted], &sl.vb.counters[CNT_P], C, ctx->scene.perm, ps);
+        ctx->launches += 1;
+    }
     mark(5, ps);
     launch_ranges(sl.sb.keys[sorted], &sl.vb.counters[CNT_P], C, sl.ranges, vp.tiles_x * vp.tiles_y, vp.key_db, ps);
     mark(6, ps);
@@ -575,7 +580,7 @@ void aaa_destroy(aaa_ctx* ctx) {
     if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
     if (ctx->rstream) cudaStreamSynchronize(ctx->rstream);
     SceneDev& s = ctx->scene;
-    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
+    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh); cudaFree(s.perm);
     for (auto& sl : ctx->slot) free_slot(sl);
     cudaFree(ctx->rec); cudaFree(ctx->rec_n); cudaFree(ctx->bwd_acc); cudaFree(ctx->bwd_overflow);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
@@ -617,6 +622,64 @@ aaa_status aaa_set_config(aaa_ctx* ctx, const aaa_config* c) {
     return AAA_OK;
 }
 
+// Store the validated scene in Morton order of its means (SceneDev::perm): AABB (per-block partial
+// min/max, reduced on the host), 30-bit codes, the onesweep sort, one gather per array. The
+// caller's index of internal Gaussian i is perm[i]; ctx->h_perm keeps a host copy for the debug
+// records.
+aaa_status reorder_scene(aaa_ctx* ctx, cudaStream_t st) {
+    SceneDev& s = ctx->scene;
+    const int64_t n = s.n;
+    const int blk = aabb_blocks(n);
+    float* d_blk = nullptr;
+    CU(cudaMalloc(&d_blk, (size_t)blk * 6 * sizeof(float)));
+    launch_aabb(s, d_blk, st);
+    std::vector<float> hb((size_t)blk * 6);
+    CU(cudaMemcpyAsync(hb.data(), d_blk, hb.size() * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFree(d_blk);
+    float lh[6] = {hb[0], hb[1], hb[2], hb[3], hb[4], hb[5]};
+    for (int b = 1; b < blk; b++)
+        for (int k = 0; k < 3; k++) {
+            lh[k] = std::min(lh[k], hb[6 * b + k]);
+            lh[3 + k] = std::max(lh[3 + k], hb[6 * b + 3 + k]);
+        }
+    SortBufs sb{};
+    uint32_t* d_count = nullptr;
+    const uint32_t cap = (uint32_t)n;
+    for (int i = 0; i < 2; i++) {
+        CU(cudaMalloc(&sb.keys[i], (size_t)cap * sizeof(skey_t)));
+        CU(cudaMalloc(&sb.vals[i], (size_t)cap * sizeof(uint32_t)));
+    }
+    CU(cudaMalloc(&sb.hist, 256 * 8 * sizeof(uint32_t)));
+    CU(cudaMalloc(&sb.tickets, 8 * sizeof(uint32_t)));
+    CU(cudaMalloc(&sb.state, sort_state_words(cap, 4) * sizeof(uint32_t)));
+    CU(cudaMalloc(&d_count, sizeof(uint32_t)));
+    CU(cudaMemcpyAsync(d_count, &cap, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    launch_morton_order(s, sb.keys[0], sb.vals[0], lh, st);
+    const int cur = launch_sort(sb, d_count, cap, 32, st);
+    uint32_t* perm = sb.vals[cur];
+    float4 *a2 = nullptr, *b2 = nullptr, *c2 = nullptr, *sh2 = nullptr;
+    CU(cudaMalloc(&a2, (size_t)n * sizeof(float4)));
+    CU(cudaMalloc(&b2, (size_t)n * sizeof(float4)));
+    CU(cudaMalloc(&c2, (size_t)n * sizeof(float4)));
+    CU(cudaMalloc(&sh2, (size_t)n * s.sh_chunks * sizeof(float4)));
+    launch_permute(s.geomA, a2, perm, n, 1, st);
+    launch_permute(s.geomB, b2, perm, n, 1, st);
+    launch_permute(s.geomC, c2, perm, n, 1, st);
+    launch_permute(s.sh, sh2, perm, n, s.sh_chunks, st);
+    CU(cudaGetLastError());
+    ctx->h_perm.resize((size_t)n);
+    CU(cudaMemcpyAsync(ctx->h_perm.data(), perm, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
+    s.geomA = a2; s.geomB = b2; s.geomC = c2; s.sh = sh2;
+    s.perm = perm;
+    cudaFree(sb.vals[cur ^ 1]);
+    for (int i = 0; i < 2; i++) cudaFree(sb.keys[i]);
+    cudaFree(sb.hist); cudaFree(sb.tickets); cudaFree(sb.state); cudaFree(d_count);
+    return AAA_OK;
+}
+
 aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* first_bad) {
     if (!ctx || !g) return AAA_ERR_INVALID_ARG;
     if (first_bad) *first_bad = -1;
@@ -632,7 +695,7 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
     }
     cudaStream_t st = ctx->stream;
     SceneDev& s = ctx->scene;
-    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh);
+    cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh); cudaFree(s.perm);
     s = SceneDev{};
     ctx->loaded = false;
     ctx->saved = false;
@@ -687,6 +750,13 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
                  (long long)bad);
         return fail(ctx, AAA_ERR_INVALID_GAUSSIAN, msg);
     }
+    ctx->h_perm.clear();
+#ifndef AAA_NO_REORDER
+    if (n > 1) {
+        aaa_status rs = reorder_scene(ctx, st);
+        if (rs) return rs;
+    }
+#endif
     ctx->loaded = true;
     return AAA_OK;
 }
@@ -906,6 +976,20 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
     *len = bytes;
     if (bytes > cap) return fail(ctx, AAA_ERR_INVALID_ARG, "debug buffer too small");
     if (bytes && src) CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    // records and indices in the caller's Gaussian order (the scene is stored in Morton order)
+    const std::vector<uint32_t>& pm = ctx->h_perm;
+    if (bytes && !pm.empty()) {
+        if (what == AAA_DBG_GAUSS || what == AAA_DBG_RASTER || what == AAA_DBG_COLOR) {
+            const size_t row = bytes / (size_t)ctx->scene.n;
+            std::vector<unsigned char> tmp(bytes);
+            const unsigned char* in = static_cast<const unsigned char*>(dst);
+            for (size_t i = 0; i < (size_t)ctx->scene.n; i++) memcpy(&tmp[(size_t)pm[i] * row], in + i * row, row);
+            memcpy(dst, tmp.data(), bytes);
+        } else if (what == AAA_DBG_VALS || what == AAA_DBG_VALS_UNSORTED) {
+            uint32_t* v = static_cast<uint32_t*>(dst);
+            for (size_t i = 0; i < bytes / 4; i++) v[i] = (v[i] & ~VAL_INDEX_MASK) | pm[v[i] & VAL_INDEX_MASK];
+        }
+    }
     return AAA_OK;
 }
 

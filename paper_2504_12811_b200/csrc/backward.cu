@@ -188,11 +188,12 @@ __global__ void __launch_bounds__(64) k_bwd_gaussians(SceneDev sc, ViewParams vp
     double grad[ND];
 #pragma unroll
     for (int i = 0; i < ND; i++) grad[i] = 0.0;
-    float* dsh = ba.d_sh + (size_t)g * K * 3;
+    const int64_t go = sc.perm ? (int64_t)sc.perm[g] : g;  // the caller's index of Gaussian g
+    float* dsh = ba.d_sh + (size_t)go * K * 3;
     if (!any) {
-        for (int i = 0; i < 3; i++) ba.d_means[3 * g + i] = 0.f, ba.d_scales[3 * g + i] = 0.f;
-        for (int i = 0; i < 4; i++) ba.d_quats[4 * g + i] = 0.f;
-        ba.d_opac[g] = 0.f;
+        for (int i = 0; i < 3; i++) ba.d_means[3 * go + i] = 0.f, ba.d_scales[3 * go + i] = 0.f;
+        for (int i = 0; i < 4; i++) ba.d_quats[4 * go + i] = 0.f;
+        ba.d_opac[go] = 0.f;
         for (int i = 0; i < 3 * K; i++) dsh[i] = 0.f;
         return;
     }
@@ -295,10 +296,10 @@ __global__ void __launch_bounds__(64) k_bwd_gaussians(SceneDev sc, ViewParams vp
         addg(v, u);
         for (int k = 0; k < K; k++) dsh[3 * k + ch] = (float)((double)u * b[k].v);
     }
-    for (int i = 0; i < 3; i++) ba.d_means[3 * g + i] = (float)grad[i];
-    for (int i = 0; i < 3; i++) ba.d_scales[3 * g + i] = (float)grad[3 + i];
-    for (int i = 0; i < 4; i++) ba.d_quats[4 * g + i] = (float)grad[6 + i];
-    ba.d_opac[g] = (float)grad[10];
+    for (int i = 0; i < 3; i++) ba.d_means[3 * go + i] = (float)grad[i];
+    for (int i = 0; i < 3; i++) ba.d_scales[3 * go + i] = (float)grad[3 + i];
+    for (int i = 0; i < 4; i++) ba.d_quats[4 * go + i] = (float)grad[6 + i];
+    ba.d_opac[go] = (float)grad[10];
 }
 
 __global__ void k_max_u32(const uint32_t* __restrict__ a, size_t n, uint32_t* out) {

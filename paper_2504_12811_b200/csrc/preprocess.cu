@@ -14,6 +14,8 @@
 // Geometry runs in FP64 (B200 has full-rate-class FP64 for this per-Gaussian work).
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "aaa_internal.cuh"
 #include "geom.cuh"
 
@@ -58,6 +60,80 @@ void launch_load_pack(const aaa_gaussians& in, const float* dm, const float* ds,
     unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
     k_load_pack<<<blocks, threads, 0, st>>>(sc.n, sc.sh_degree, dm, ds, dq, dop, dsh, dvt, sc.geomA, sc.geomB,
                                             sc.geomC, sc.sh, sc.sh_chunks, (unsigned long long*)d_bad);
+}
+
+// ------------------------------------------------------------------ L0: spatial order
+// Morton (Z-order) codes of the means over the scene's bounding box, 10 bits per axis: sorting
+// the scene by them at load puts spatially close Gaussians in the same warps of K1 (coherent
+// culling and bounds branches) and next to each other in memory (K6 gathers their records).
+__global__ void __launch_bounds__(256) k_aabb(const float4* __restrict__ A, int64_t n, float* __restrict__ out) {
+    float lo[3] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F}, hi[3] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 a = __ldg(&A[i]);
+        lo[0] = fminf(lo[0], a.x); lo[1] = fminf(lo[1], a.y); lo[2] = fminf(lo[2], a.z);
+        hi[0] = fmaxf(hi[0], a.x); hi[1] = fmaxf(hi[1], a.y); hi[2] = fmaxf(hi[2], a.z);
+    }
+    __shared__ float s[6][8];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+            hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 3; k++) s[k][w] = lo[k], s[3 + k][w] = hi[k];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[threadIdx.x][0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); i++)
+            v = threadIdx.x < 3 ? fminf(v, s[threadIdx.x][i]) : fmaxf(v, s[threadIdx.x][i]);
+        out[blockIdx.x * 6 + threadIdx.x] = v;
+    }
+}
+
+int aabb_blocks(int64_t n) { return (int)std::min<int64_t>(1024, (n + 255) / 256); }
+
+void launch_aabb(const SceneDev& sc, float* d_blk, cudaStream_t st) {
+    k_aabb<<<aabb_blocks(sc.n), 256, 0, st>>>(sc.geomA, sc.n, d_blk);
+}
+
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_morton(const float4* __restrict__ A, int64_t n, float lx, float ly, float lz, float sx, float sy,
+                         float sz, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 a = __ldg(&A[i]);
+    auto q = [](float v) { return (uint32_t)fminf(fmaxf(v, 0.f), 1023.f); };
+    keys[i] = spread10(q((a.x - lx) * sx)) | (spread10(q((a.y - ly) * sy)) << 1) | (spread10(q((a.z - lz) * sz)) << 2);
+    vals[i] = (uint32_t)i;
+}
+
+void launch_morton_order(const SceneDev& sc, uint32_t* keys, uint32_t* vals, const float* lh, cudaStream_t st) {
+    auto sc_of = [](float lo, float hi) { return hi > lo ? 1023.f / (hi - lo) : 0.f; };
+    k_morton<<<(unsigned)((sc.n + 255) / 256), 256, 0, st>>>(sc.geomA, sc.n, lh[0], lh[1], lh[2], sc_of(lh[0], lh[3]),
+                                                             sc_of(lh[1], lh[4]), sc_of(lh[2], lh[5]), keys, vals);
+}
+
+// out[c * n + i] = in[c * n + perm[i]] for each of `chunks` SoA chunks
+__global__ void k_permute(const float4* __restrict__ in, float4* __restrict__ out, const uint32_t* __restrict__ perm,
+                          int64_t n, int chunks) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t p = perm[i];
+    for (int c = 0; c < chunks; c++) out[(int64_t)c * n + i] = __ldg(&in[(int64_t)c * n + p]);
+}
+
+void launch_permute(const float4* in, float4* out, const uint32_t* perm, int64_t n, int chunks, cudaStream_t st) {
+    if (n > 0) k_permute<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, perm, n, chunks);
 }
 
 // ------------------------------------------------------------------ K1 helpers

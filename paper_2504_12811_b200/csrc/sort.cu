@@ -192,6 +192,38 @@ int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bit
     return cur;
 }
 
+// Global-order ablations (AAA_FLAG_NO_HIER_SORT / NO_3D): the list order among equal keys is the
+// blend order, and its tie rule is the caller's Gaussian index (DESIGN readings). The scene is
+// stored in Morton order, so each run of equal keys (short: equal tile and mean-depth code) is
+// re-sorted by the caller's index perm[g]; the exact mode needs no fix (its per-pixel order is by
+// z*, ties are ambiguous at the oracle's resolution).
+__global__ void k_tie_fix(const skey_t* __restrict__ keys, uint32_t* vals, const uint32_t* d_count,
+                          const uint32_t* __restrict__ perm) {
+    const uint32_t P = *d_count;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        const skey_t k = keys[i];
+        if (i > 0 && keys[i - 1] == k) continue;           // not the start of a run
+        if (i + 1 >= P || keys[i + 1] != k) continue;        // run of one
+        uint32_t j = i + 1;
+        while (j < P && keys[j] == k) j++;
+        for (uint32_t a = i + 1; a < j; a++) {                // insertion sort by the caller's index
+            const uint32_t v = vals[a], pv = perm[v & VAL_INDEX_MASK];
+            uint32_t b = a;
+            while (b > i && perm[vals[b - 1] & VAL_INDEX_MASK] > pv) {
+                vals[b] = vals[b - 1];
+                b--;
+            }
+            vals[b] = v;
+        }
+    }
+}
+
+void launch_tie_fix(const skey_t* keys, uint32_t* vals, const uint32_t* d_count, uint32_t cap, const uint32_t* perm,
+                    cudaStream_t st) {
+    if (cap == 0 || !perm) return;
+    k_tie_fix<<<min((cap + 255) / 256, 148u * 8u), 256, 0, st>>>(keys, vals, d_count, perm);
+}
+
 // ------------------------------------------------------------------ K5: tile ranges
 __global__ void k_ranges(const skey_t* __restrict__ keys, const uint32_t* d_count, uint2* ranges, int key_db) {
     uint32_t P = *d_count;

@@ -12,7 +12,8 @@ constexpr int VT_THREADS = 256, VT_CAMS = 128;
 
 __global__ void __launch_bounds__(VT_THREADS) k_vtrain(const float4* __restrict__ geomA, int64_t n,
                                                        const VtCam* __restrict__ cams, int n_cams,
-                                                       float* __restrict__ out, float4* geomB_store) {
+                                                       float* __restrict__ out, float4* geomB_store,
+                                                       const uint32_t* __restrict__ perm) {
     __shared__ VtCam s_cam[VT_CAMS];
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double mu[3] = {0.0, 0.0, 0.0};
@@ -39,14 +40,14 @@ __global__ void __launch_bounds__(VT_THREADS) k_vtrain(const float4* __restrict_
     }
     if (g >= n) return;
     const float v = best > 0.0 ? (float)best : CUDART_INF_F;
-    if (out) out[g] = v;
+    if (out) out[perm ? (int64_t)perm[g] : g] = v;  // the caller's order
     if (geomB_store) geomB_store[g].w = v;
 }
 
 void launch_vtrain(const SceneDev& sc, const VtCam* cams, int n_cams, float* out, bool store, cudaStream_t st) {
     if (sc.n == 0) return;
     const unsigned blocks = (unsigned)((sc.n + VT_THREADS - 1) / VT_THREADS);
-    k_vtrain<<<blocks, VT_THREADS, 0, st>>>(sc.geomA, sc.n, cams, n_cams, out, store ? sc.geomB : nullptr);
+    k_vtrain<<<blocks, VT_THREADS, 0, st>>>(sc.geomA, sc.n, cams, n_cams, out, store ? sc.geomB : nullptr, sc.perm);
 }
 
 }  // namespace aaa
