@@ -56,23 +56,28 @@ def main():
     rows = [x for x in csv.reader(open(OUT / f"launches_{r}.csv")) if len(x) > 10]
     h, rows = rows[0], rows[1:]
     agg = OrderedDict()
+    load = OrderedDict()  # scene load (validation, pack, Morton order): every launch before the first K1
+    seen_k1 = False
     for x in rows:
         d = dict(zip(h, x))
-        agg.setdefault(base(d["Kernel Name"]), []).append(float(d["Metric Value"]) / 1e3)  # us
+        k = base(d["Kernel Name"])
+        seen_k1 = seen_k1 or k == "k_preprocess"
+        (agg if seen_k1 else load).setdefault(k, []).append(float(d["Metric Value"]) / 1e3)  # us
     n_views = len(agg.get("k_preprocess", [1]))
-    per_view = {k: sum(v) / n_views for k, v in agg.items() if k != "k_load_pack"}
+    per_view = {k: sum(v) / n_views for k, v in agg.items()}
     tot = sum(per_view.values())
     lines = [f"# {r}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
              "Command: `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 "
              "--warmup 3 --views-per-rank 4 --no-cpu-baseline --no-e2e` (c3: 3M Gaussians, 1920x1080). "
              "Per-launch times are cold-cache and serialised; compare the SHARE of a view with bench.py's "
              "`stages`.", "",
-             f"{len(rows)} launches, {n_views} views.", "",
+             f"{len(rows)} launches ({sum(len(v) for v in load.values())} at scene load), {n_views} views.", "",
              "| kernel | launches | mean us/launch | us per view | share of view |", "|---|---|---|---|---|"]
+    for k, v in load.items():
+        lines.append(f"| {k} (scene load) | {len(v)} | {sum(v) / len(v):.1f} | (load, once) | |")
     for k, v in agg.items():
-        pv = per_view.get(k)
-        lines.append(f"| {k} | {len(v)} | {sum(v) / len(v):.1f} | {pv:.1f} | {pv / tot:.1%} |" if pv is not None
-                     else f"| {k} | {len(v)} | {sum(v) / len(v):.1f} | (load, once) | |")
+        pv = per_view[k]
+        lines.append(f"| {k} | {len(v)} | {sum(v) / len(v):.1f} | {pv:.1f} | {pv / tot:.1%} |")
     lines += ["", f"Sum per view: {tot / 1e3:.3f} ms."]
     (PROF / f"{r}_launches.md").write_text("\n".join(lines) + "\n")
     # ---- full capture
