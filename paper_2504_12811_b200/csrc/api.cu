@@ -318,7 +318,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     s = ensure_tiles(ctx, sl, vp.tiles_x * vp.tiles_y);
     if (s) return s;
     if (debug_k1 && !sl.vb.dbg)
-        CU(cudaMalloc(&sl.vb.dbg, (size_t)(n > 0 ? n : 1) * AAA_DBG_GAUSS_FIELDS * sizeof(double)));
+        CU(cudaMalloc(&sl.vb.dbg, (size_t)(sl.vb_n > 0 ? sl.vb_n : 1) * AAA_DBG_GAUSS_FIELDS * sizeof(double)));  // slot capacity (>= n)
     CU(grow(sl.vb.scan_state, sl.scan_state_cap, scan_state_words(n) + 8));
     const bool timing = (ctx->cfg.flags & AAA_FLAG_TIMING) != 0 && stop_after == 0;
     cudaEvent_t* ev = nullptr;
