@@ -196,7 +196,7 @@ int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bit
 // blend order, and its tie rule is the caller's Gaussian index (DESIGN readings). The scene is
 // stored in Morton order, so each run of equal keys (short: equal tile and mean-depth code) is
 // re-sorted by the caller's index perm[g]; the exact mode needs no fix (its per-pixel order is by
-// z*, ties are ambiguous at the oracle's resolution).
+// z*; exact float ties are order-ambiguous by definition, reading 4).
 __global__ void k_tie_fix(const skey_t* __restrict__ keys, uint32_t* vals, const uint32_t* d_count,
                           const uint32_t* __restrict__ perm) {
     const uint32_t P = *d_count;
