@@ -589,3 +589,96 @@ def test_2d_splat_mode_closed_form_and_jacobian():
             else:
                 assert want > orc.gaussians()[0, O.G_FIELDS.index("tau")] - 1e-3
     assert n_hit > 3
+
+
+# ---------------------------------------------------------------- camera-inside and tau level set
+def _alpha_level_rho2(oA):
+    """The rho^2 at which alpha(rho^2) = oA exp(-rho^2/2) (Eq. 9 with amplitude A) falls to 1/255
+    (reading 1: the tau-ellipsoid is the alpha >= 1/255 level set), found by bisection on the
+    alpha curve itself — not the closed form."""
+    lo, hi = 0.0, 200.0
+    for _ in range(200):
+        m = 0.5 * (lo + hi)
+        if oA * math.exp(-0.5 * m) >= 1.0 / 255.0:
+            lo = m
+        else:
+            hi = m
+    return 0.5 * (lo + hi)
+
+
+def test_camera_inside_discard_on_filtered_ellipsoid():
+    """P:292 (reading 8): a Gaussian whose FILTERED tau-ellipsoid contains the camera is discarded.
+    The camera is put at Mahalanobis distance (1 -/+ 2%) of the level set along a random ray: with
+    v' = v_train (the camera is close, so v_hat > v_train) Sigma_hat and A do not change along the
+    ray, and the camera's Gaussian-space point is lambda M^-1 dir (M from helpers.filtered_T_view,
+    the paper's T_view with filtered scales, P:283). Just inside -> discarded (background image);
+    just outside -> kept. Fails if the oracle tested Sigma instead of Sigma_hat, or dropped the 2 of
+    tau (both checked once by mutation)."""
+    rng = np.random.default_rng(77)
+    cam = pinhole(W=32, H=32, f=56.0)
+    n_in = n_out = 0
+    for trial in range(40):
+        s = np.exp(rng.uniform(np.log(0.03), np.log(0.3), 3))
+        q = rng.standard_normal(4)
+        d = rng.standard_normal(3)
+        d[2] = abs(d[2]) + 0.5
+        d /= np.linalg.norm(d)
+        o = rng.uniform(0.3, 0.95)
+        probe = one_gaussian(d, s, q=q, o=o, v_train=3.0)
+        M, muv, shat, R = filtered_T_view(probe, 0, cam)
+        assert 56.0 / muv[2] > 3.0 and np.isclose(shat[0], s[0] ** 2 + 0.3 / 9.0)  # v' = v_train
+        A = eq12_amplitude(s, shat, R, d)
+        lam_star = math.sqrt(_alpha_level_rho2(o * A)) / np.linalg.norm(np.linalg.solve(M, d))
+        for fac, inside in ((0.98, True), (1.02, False)):
+            mu = fac * lam_star * d
+            sc = one_gaussian(mu, s, q=q, o=o, v_train=3.0)
+            M2, muv2, shat2, _ = filtered_T_view(sc, 0, cam)
+            if 56.0 / muv2[2] <= 3.0:
+                continue  # filter would depend on the distance; keep the construction exact
+            orc = O.Oracle(sc).set_view(cam)
+            G = orc.gaussians()[0]
+            assert bool(G[FI["inside"]]) == inside, (trial, fac, G[FI["inside_rho2"]], G[FI["tau"]])
+            assert bool(G[FI["valid"]]) == (not inside)
+            if inside:
+                img = orc.render_image()[0]
+                np.testing.assert_array_equal(img[..., 3], 1.0)
+                n_in += 1
+            else:
+                n_out += 1
+    assert n_in >= 20 and n_out >= 20
+
+
+def test_tau_level_set_per_pixel():
+    """P:276/P:312 with reading 1: a pixel receives a contribution iff alpha = o A exp(-rho^2/2)
+    >= 1/255, rho^2 from the paper's plane pullback (Eq. 4-5, helpers.plane_form_rho2) and A from
+    Eq. 12 (helpers.eq12_amplitude). Pixels straddle the boundary on both sides; a pixel counts as
+    receiving a contribution iff its transmittance drops below 1. Fails if tau loses its factor 2
+    or uses o instead of o A (checked once by mutation)."""
+    rng = np.random.default_rng(5)
+    cam = pinhole(W=96, H=96, f=120.0)
+    n_straddle_in = n_straddle_out = 0
+    for trial in range(6):
+        s = np.exp(rng.uniform(np.log(0.05), np.log(0.25), 3))
+        q = rng.standard_normal(4)
+        mu = np.array([rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), rng.uniform(2.5, 4.0)])
+        o = rng.uniform(0.4, 0.95)
+        sc = one_gaussian(mu, s, q=q, o=o, v_train=8.0)
+        M, muv, shat, R = filtered_T_view(sc, 0, cam)
+        A = eq12_amplitude(s, shat, R, mu / np.linalg.norm(mu))
+        assert A < 0.97  # the filter is active, so o and o A differ
+        orc = O.Oracle(sc).set_view(cam)
+        yy, xx = np.mgrid[0:cam.height, 0:cam.width]
+        rgbT = orc.render_pixels(xx.ravel(), yy.ravel())[0]
+        for idx in range(xx.size):
+            px, py = xx.ravel()[idx], yy.ravel()[idx]
+            rho2, z = plane_form_rho2(M, muv, cam, px + 0.5, py + 0.5)
+            a = o * A * math.exp(-0.5 * rho2)
+            margin = a * 255.0 - 1.0
+            if abs(margin) < 1e-9:
+                continue
+            hit = rgbT[idx, 3] < 1.0
+            assert hit == (margin > 0), (trial, px, py, rho2, a)
+            if abs(margin) < 0.5:
+                n_straddle_in += margin > 0
+                n_straddle_out += margin < 0
+    assert n_straddle_in >= 50 and n_straddle_out >= 50
