@@ -33,6 +33,9 @@ extern "C" {
 #endif
 
 typedef enum {
+    AAA_WARN_UNRESOLVED = 1,       /* results written, but some pixels of the last view hit a
+                                      full spill queue and hold a partial (inexact) blend; only
+                                      aaa_get_stats / aaa_synchronize return it (stats filled) */
     AAA_OK = 0,
     AAA_ERR_INVALID_ARG = -1,      /* null pointer, bad camera/config value, bad sizes      */
     AAA_ERR_INVALID_GAUSSIAN = -2, /* load-time validation failed; see first_bad   */
@@ -216,7 +219,10 @@ aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_ca
 aaa_status aaa_render_backward(aaa_ctx* ctx, const float* dL_drgb, const float* dL_dT, float* d_means,
                                float* d_scales, float* d_quats, float* d_opac, float* d_sh);
 
-aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out); /* synchronises */
+/* Both synchronise; both return AAA_WARN_UNRESOLVED (stats still filled) when pixels of the last
+ * view were left inexact because a spill queue was full (stats.unresolved_pixels; never seen on
+ * c1-c5). */
+aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out);
 aaa_status aaa_synchronize(aaa_ctx* ctx);
 
 /* Copy an internal buffer of the last render to host memory (parity tests only). *len

@@ -199,5 +199,9 @@ void launch_aabb(const SceneDev& sc, float* d_blk, cudaStream_t st);
 void launch_permute(const float4* in, float4* out, const uint32_t* perm, int64_t n, int chunks, cudaStream_t st);
 void launch_vtrain(const SceneDev& sc, const VtCam* cams, int n_cams, float* out, bool store, cudaStream_t st);
 void launch_raster_fallback(const ViewParams& vp, const RasterArgs& ra, cudaStream_t st);
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set it once per (kernel, device, size)
+// for the current device (thread-safe); a failure is returned and also left in cudaGetLastError()
+// for the launching entry point to report.
+cudaError_t ensure_smem_attr(const void* func, size_t bytes);
 
 }  // namespace aaa

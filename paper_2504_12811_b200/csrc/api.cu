@@ -14,12 +14,29 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "aaa_internal.cuh"
 
 using namespace aaa;
+
+cudaError_t aaa::ensure_smem_attr(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, size_t>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(func, dev, bytes);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
 
 namespace {
 
@@ -100,6 +117,9 @@ aaa_status fail(aaa_ctx* c, aaa_status s, const std::string& m) {
             return fail(ctx, e_ == cudaErrorMemoryAllocation ? AAA_ERR_OOM : AAA_ERR_CUDA,        \
                         std::string(#expr) + ": " + cudaGetErrorString(e_));                      \
     } while (0)
+
+// every entry point that allocates, launches or synchronises first selects the context's device
+#define SETDEV(ctx) CU(cudaSetDevice((ctx)->device))
 
 template <typename T>
 cudaError_t grow(T*& p, size_t& cap, size_t need) {
@@ -462,6 +482,17 @@ aaa_status leave(aaa_ctx* ctx) {
     return AAA_OK;
 }
 
+// AAA_WARN_UNRESOLVED when a pixel of the last view could not be finished exactly (spill queue
+// full: the pixel holds its partial state); needs the streams synchronised
+aaa_status unresolved_status(aaa_ctx* ctx) {
+    const Slot& sl = ctx->slot[ctx->cur];
+    if (!sl.vb.counters) return AAA_OK;
+    uint32_t u = 0;
+    CU(cudaMemcpy(&u, &sl.vb.counters[CNT_UNRESOLVED], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (u) return fail(ctx, AAA_WARN_UNRESOLVED, std::to_string(u) + " pixels unresolved (spill queue full); they hold a partial blend");
+    return AAA_OK;
+}
+
 aaa_status sync_all(aaa_ctx* ctx) {
     CU(cudaStreamSynchronize(ctx->pstream));
     CU(cudaStreamSynchronize(ctx->rstream));
@@ -577,6 +608,7 @@ aaa_status aaa_create(int32_t device, void* stream, aaa_ctx** out) {
 
 void aaa_destroy(aaa_ctx* ctx) {
     if (!ctx) return;
+    cudaSetDevice(ctx->device);
     if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
     if (ctx->rstream) cudaStreamSynchronize(ctx->rstream);
     SceneDev& s = ctx->scene;
@@ -795,6 +827,7 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
     if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
     const int ty = (ctx->cam.height + TILE - 1) / TILE;
     if (n_rows < ty) return fail(ctx, AAA_ERR_INVALID_ARG, "n_rows < tile rows");
+    SETDEV(ctx);
     aaa_status s = run_debug_view(ctx, false);
     if (s) return s;
     const Slot& sl = ctx->slot[ctx->cur];
@@ -813,6 +846,7 @@ aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_ca
     if (!ctx->loaded) return fail(ctx, AAA_ERR_STATE, "aaa_compute_vtrain before aaa_load_gaussians");
     if (n_cams < 0 || (n_cams > 0 && !cams)) return fail(ctx, AAA_ERR_INVALID_ARG, "need n_cams >= 0 cameras");
     if (!out && !store) return fail(ctx, AAA_ERR_INVALID_ARG, "out is null and store == 0");
+    SETDEV(ctx);
     std::vector<VtCam> h(n_cams > 0 ? n_cams : 1);
     for (int i = 0; i < n_cams; i++) {
         aaa_status s = check_camera(ctx, &cams[i]);
@@ -840,6 +874,7 @@ aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_ca
     float* d_out = dev_out ? out : nullptr;
     if (out && !dev_out && bytes) CU(cudaMalloc(&d_out, bytes));
     launch_vtrain(ctx->scene, d_cams, n_cams, d_out, store != 0, st);
+    if (store) ctx->saved = false;  // a saved render's K1 state no longer matches v_train
     CU(cudaGetLastError());
     if (out && !dev_out && bytes) CU(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -854,6 +889,7 @@ aaa_status aaa_render_backward(aaa_ctx* ctx, const float* dL_drgb, const float* 
     if (!ctx->saved) return fail(ctx, AAA_ERR_STATE, "no render saved with AAA_FLAG_SAVE_CONTRIBS");
     if (!dL_drgb || !d_means || !d_scales || !d_quats || !d_opac || !d_sh)
         return fail(ctx, AAA_ERR_INVALID_ARG, "null pointer");
+    SETDEV(ctx);
     const Slot& sl = ctx->slot[ctx->cur];
     const int64_t n = ctx->scene.n;
     CU(grow(ctx->bwd_acc, ctx->bwd_acc_cap, (size_t)(n > 0 ? n : 1) * BWD_ACC));
@@ -887,6 +923,7 @@ aaa_status aaa_render_backward(aaa_ctx* ctx, const float* dL_drgb, const float* 
 
 aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     if (!ctx || !out) return AAA_ERR_INVALID_ARG;
+    SETDEV(ctx);
     {
         aaa_status s = sync_all(ctx);
         if (s) return s;
@@ -931,17 +968,23 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     ctx->ev_used = 0;
     out->timed_views = nv;
     for (int i = 0; i < 10; i++) out->ms[i] = nv ? (float)(acc[i] / nv) : 0.f;
-    return AAA_OK;
+    return out->unresolved_pixels ? fail(ctx, AAA_WARN_UNRESOLVED, std::to_string(out->unresolved_pixels) +
+                                                                       " pixels unresolved (spill queue full)")
+                                  : AAA_OK;
 }
 
 aaa_status aaa_synchronize(aaa_ctx* ctx) {
     if (!ctx) return AAA_ERR_INVALID_ARG;
-    return sync_all(ctx);
+    SETDEV(ctx);
+    aaa_status s = sync_all(ctx);
+    if (s) return s;
+    return unresolved_status(ctx);
 }
 
 aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, size_t* len) {
     if (!ctx || !dst || !len) return AAA_ERR_INVALID_ARG;
     if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
+    SETDEV(ctx);
     aaa_status s = AAA_OK;
     if (what == AAA_DBG_GAUSS || what == AAA_DBG_KEYS_UNSORTED || what == AAA_DBG_VALS_UNSORTED)
         s = run_debug_view(ctx, what == AAA_DBG_GAUSS);

@@ -176,11 +176,7 @@ int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bit
     unsigned hblocks = min(blocks, 148u * 4u);
     k_sort_hist<<<hblocks, 256, 0, st>>>(sb.keys[0], d_count, passes, sb.hist);
     k_sort_hist_scan<<<passes, 256, 0, st>>>(sb.hist);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)onesweep_smem());
-        attr = true;
-    }
+    if (ensure_smem_attr((const void*)k_onesweep, onesweep_smem()) != cudaSuccess) return 0;
     int cur = 0;
     for (int p = 0; p < passes; p++) {
         k_onesweep<<<blocks, SORT_THREADS, onesweep_smem(), st>>>(sb.keys[cur], sb.vals[cur], sb.keys[cur ^ 1],

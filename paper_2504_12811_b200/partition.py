@@ -26,11 +26,14 @@ def view_shard(n_views: int, rank: int, world: int) -> list[int]:
 
 def band_split(row_costs, world: int) -> list[tuple[int, int]]:
     """Split tile rows [0, R) into `world` contiguous bands of near-equal cost (prefix-sum
-    cut points); every band gets >= 1 row when R >= world. Identical on every rank."""
+    cut points); every band gets >= 1 row. Identical on every rank. world > R is rejected
+    (an empty band cannot be rendered by aaa_render_tiles)."""
     c = np.asarray(row_costs, dtype=np.float64)
     R = c.shape[0]
-    if world <= 1 or R == 0:
+    if world <= 1:
         return [(0, R)]
+    if world > R:
+        raise ValueError(f"band_split: {world} bands need at least {world} tile rows (have {R})")
     pref = np.concatenate([[0.0], np.cumsum(c + 1e-9)])   # +eps: empty rows still count a little
     total = pref[-1]
     cuts = [0]
@@ -39,7 +42,7 @@ def band_split(row_costs, world: int) -> list[tuple[int, int]]:
         r = int(np.searchsorted(pref, target))
         lo = cuts[-1] + 1
         hi = R - (world - k)
-        cuts.append(int(min(max(r, lo), hi)) if R >= world else min(k, R))
+        cuts.append(int(min(max(r, lo), hi)))
     cuts.append(R)
     return [(cuts[i], cuts[i + 1]) for i in range(world)]
 
@@ -110,7 +113,7 @@ def gather_bands(band_rgb, bands, width: int, height: int, rank: int, world: int
     with one NCCL all-gather of equal-size padded bands."""
     import torch
     import torch.distributed as dist
-    max_h = max(min(16 * b, height) - 16 * a for a, b in bands)
+    max_h = max(max(0, min(16 * b, height) - 16 * a) for a, b in bands)
     pad = torch.zeros((3, max_h, width), dtype=band_rgb.dtype, device=band_rgb.device)
     pad[:, : band_rgb.shape[1]] = band_rgb
     out = torch.empty((world * 3, max_h, width), dtype=band_rgb.dtype, device=band_rgb.device)
@@ -120,6 +123,6 @@ def gather_bands(band_rgb, bands, width: int, height: int, rank: int, world: int
         return None
     parts = []
     for r, (a, b) in enumerate(bands):
-        h = min(16 * b, height) - 16 * a
+        h = max(0, min(16 * b, height) - 16 * a)
         parts.append(out[r, :, :h])
     return torch.cat(parts, dim=1)

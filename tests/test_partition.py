@@ -37,6 +37,13 @@ def test_band_split_balanced_contiguous(world):
     assert max(loads) <= costs.sum() / world + costs.max() + 1e-6
 
 
+def test_band_split_rejects_more_bands_than_rows():
+    """An empty band cannot be rendered (aaa_render_tiles rejects it): world > R is an error."""
+    with pytest.raises(ValueError):
+        part.band_split(np.ones(3), 4)
+    assert part.band_split(np.ones(4), 4) == [(0, 1), (1, 2), (2, 3), (3, 4)]
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
