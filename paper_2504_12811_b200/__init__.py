@@ -255,5 +255,9 @@ class Renderer:
         n_tiles = ((self.width + 15) // 16) * ((self.height + 15) // 16)
         return min(32 - max(0, (n_tiles - 1).bit_length()), 28)
 
+    def spilled_pixels(self) -> np.ndarray:
+        """Linear indices (y * W + x) of the pixels of the last render continued by K6s (debug)."""
+        return self.debug_copy(AAA_DBG_SPILL, np.uint32, 8)[:, 0].copy()
+
     def ranges(self) -> np.ndarray:
         return self.debug_copy(AAA_DBG_RANGES, np.uint32, 2)

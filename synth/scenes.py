@@ -388,14 +388,32 @@ def c4_cameras(kind: str, n_views: int = 50) -> list:
     if kind == "zoomout":
         return c3_cameras(200, radius_scale=8.0)[::4][:n_views]
     if kind == "inside":
+        # 40 views dolly from the orbit into the object region, then 10 views land on the ground
+        # disc: heights log-spaced down to 4 mm, pitching down to 38 degrees, so the last views have
+        # the camera inside ground surfels and every visible Gaussian crossing the near
+        # plane (the exact 5-constraint culling path)
         cams = []
         start = np.array([4.0, 0.0, 1.5])
         end = np.array([0.0, 0.05, 0.5])      # object centre region
-        for i in range(n_views):
+        n_dolly = n_views - 10 if n_views > 20 else n_views
+        d0 = np.array([-1.0, 0.02, -0.15])
+        for i in range(n_dolly):
             t = (i / max(1, n_views - 1)) ** 0.5
             eye = (1 - t) * start + t * end
-            tgt = eye + np.array([-1.0, 0.02, -0.15])
-            cams.append(Camera(1920, 1080, 1663.0, 1663.0, 960.0, 540.0, look_at(eye, tgt), 0.01))
+            cams.append(Camera(1920, 1080, 1663.0, 1663.0, 960.0, 540.0, look_at(eye, eye + d0), 0.01))
+        if n_dolly < n_views:
+            e0 = (1 - ((n_dolly - 1) / (n_views - 1)) ** 0.5) * start + ((n_dolly - 1) / (n_views - 1)) ** 0.5 * end
+            land = np.array([2.5, 0.0, 0.004])
+            pitch = np.radians(38.0)
+            d1 = np.array([-math.cos(pitch), 0.0, -math.sin(pitch)])
+            m = n_views - n_dolly
+            for k in range(1, m + 1):
+                u = k / m
+                h = math.exp((1 - u) * math.log(e0[2]) + u * math.log(land[2]))
+                xy = (1 - u) * e0[:2] + u * land[:2]
+                eye = np.array([xy[0], xy[1], h])
+                d = (1 - u) * d0 / np.linalg.norm(d0) + u * d1
+                cams.append(Camera(1920, 1080, 1663.0, 1663.0, 960.0, 540.0, look_at(eye, eye + d), 0.01))
         return cams
     raise ValueError(kind)
 

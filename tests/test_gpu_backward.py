@@ -6,6 +6,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+import oracle as O  # noqa: E402
 import paper_2504_12811_b200 as pkg  # noqa: E402
 from oracle import autograd_ref as AR  # noqa: E402
 from synth import scenes as S  # noqa: E402
@@ -18,6 +19,27 @@ def R():
     from paper_2504_12811_b200 import _build
     _build.build()
     return pkg.Renderer(0)
+
+
+def _ambiguous_gaussians(scene, cam):
+    """Gaussians whose gradient depends on an FP32-undecidable choice: those with a flagged
+    contribution on some pixel, and those blended on a pixel after a flagged contribution (the
+    transmittance they see depends on the choice). Termination (T_eps) is a flagged choice too."""
+    orc = O.Oracle(scene).set_view(cam)
+    CI = {f: i for i, f in enumerate(O.C_FIELDS)}
+    amb = np.zeros(scene.n, bool)
+    flagged = O.F_CUTOFF | O.F_NEAR | O.F_TIE | O.F_GAUSS | O.F_TERMINATED
+    for y in range(cam.height):
+        for x in range(cam.width):
+            c = orc.pixel_contribs(x, y)
+            if len(c) == 0:
+                continue
+            fl = c[:, CI["flags"]].astype(np.int64) & flagged
+            if not fl.any():
+                continue
+            first = int(np.nonzero(fl)[0][0])
+            amb[c[first:, CI["g"]].astype(np.int64)] = True
+    return amb
 
 
 def _scenes():
@@ -45,16 +67,22 @@ def test_backward_matches_autograd(R, idx):
     finally:
         R.set_config(flags=0)
     ref = AR.grads(scene, cam, wr, wt)
+    amb = _ambiguous_gaussians(scene, cam)
     for field in ("means", "scales", "quats", "opacities", "sh"):
         a = g[field].cpu().numpy().astype(np.float64).reshape(ref[field].shape)
         b = ref[field]
         scale = np.abs(b).max()
         err = np.abs(a - b)
-        # FP32 records and atomics vs FP64: a few 1e-4 of the field's largest gradient, except the
-        # rare Gaussians with a contribution inside the FP32 cutoff band (ambiguity)
-        bad = err > 2e-3 * scale + 2e-3 * np.abs(b)
-        frac = bad.reshape(bad.shape[0], -1).any(1).mean()
-        assert frac <= 0.05, (name, field, frac, float(err.max()), float(scale))
+        # FP32 records and atomics vs FP64: within 2e-3 of the field's largest gradient (+2e-3
+        # relative) for every Gaussian whose contribution set and order are decided the same way
+        # in FP32 and FP64. A Gaussian may differ only if the oracle flags one of its own
+        # contributions, or an earlier one on the same pixel ray, as ambiguous (cutoff band, near
+        # plane, depth tie, inside margin: SURVEY 8c step 5) — the forward then blends a different
+        # admissible variant and the derivative of that variant is what the GPU returns.
+        bad = (err > 2e-3 * scale + 2e-3 * np.abs(b)).reshape(err.shape[0], -1).any(1)
+        unexplained = bad & ~amb
+        assert not unexplained.any(), (name, field, np.nonzero(unexplained)[0][:10], float(err.max()),
+                                       float(scale), int(bad.sum()), int(amb.sum()))
         assert np.median(err) <= 1e-3 * scale, (name, field)
 
 
