@@ -475,7 +475,8 @@ def _cache_dir() -> Path:
     d = os.environ.get("AAA_SCENE_CACHE")
     if d:
         return Path(d)
-    return Path(__file__).resolve().parent.parent / ".scene_cache"
+    # outside the repo, so the cached .npz bytes never travel with gpurun snapshots
+    return Path.home() / ".cache" / "aaa_scenes"
 
 
 def cached(name: str, fn, *args, **kw) -> Scene:
