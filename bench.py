@@ -1,13 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the B200 AAA-Gaussians forward renderer (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c5|...]
 
-Workload (BASELINE.json configs[2]): 3M synthetic M360-shaped Gaussians, SH
-degree 3, 1920x1080 views on a 200-view orbit. One step = every rank renders its block of
-`--views-per-rank` views (weak scaling: per-rank work fixed, views interleaved along the orbit,
-view index k*8 + rank). Scene bytes (720 MB) exceed the 126 MB L2, so every view re-streams
-its inputs from HBM (no flush needed). Prints ONE JSON line on rank 0.
+Default workload (BASELINE.json configs[2]): 3M synthetic M360-shaped Gaussians,
+SH degree 3, 1920x1080, the fixed 200-view orbit batch sharded by view over the ranks (strong
+scaling; `--scaling weak` renders `--views-per-rank` views per rank instead). One step = the whole
+batch. The scene (720 MB) exceeds the 126 MB L2, so every view re-streams its inputs from HBM (no
+flush needed). With N > 1 the NCCL gather of the images to rank 0 is timed separately (`gather`).
+`--config c5`: one 6M-Gaussian 3840x2160 frame per step, split by cost-balanced tile-row bands
+(aaa_render_band), band gather timed separately. `--gpus N` outside torchrun re-launches itself
+under torch.distributed.run (gloo with ranks sharing devices when fewer GPUs are visible).
+Prints ONE JSON line on rank 0.
 
 --impl reference times the float64 CPU oracle (oracle/) on the host cores on a bounded pixel
 sample of the same views (the tier's reference arm).
@@ -110,27 +114,114 @@ def dist_env():
     return ws, rank, local
 
 
-def scene_and_views(cfg: str, rank: int, world: int, per_rank: int):
-    from synth import scenes as S
-    scene, cams = S.make_config(cfg)
-    stride = max(8, world)
-    idx = [(k * stride + rank) % len(cams) for k in range(per_rank)]
-    return scene, cams, idx
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks (one per GPU). With fewer visible GPUs than N (a functional
+    run of the N-rank path on one device) the ranks share devices and use gloo."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    env = dict(os.environ)
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:
+        ngpu = 0
+    if ngpu < args.gpus:
+        env.setdefault("AAA_DIST_BACKEND", "gloo")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
-def stage_bytes(st, n, deg):
-    """Algorithmic bytes per view for each HBM-bound stage."""
+def fp32_peak():
+    """Measured FFMA throughput (tools/ffma_peak.cu -> profiles/fp32_peak.json): the sustained
+    figure (K6 runs inside a seconds-long step); the derived nominal figure if absent."""
+    p = ROOT / "profiles" / "fp32_peak.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["fp32_tflops_sustained"]), ("measured: tools/ffma_peak.cu sustained FFMA "
+                                                       f"(profiles/fp32_peak.json, burst {d['fp32_tflops']:.1f})")
+        except Exception:
+            pass
+    return FP32_PEAK_TFLOPS, "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (no measurement found)"
+
+
+def stage_bytes(st, n, deg, px):
+    """Algorithmic bytes per view of each stage: what the method must move.
+    V visible, C candidate pairs, P kept pairs, px pixels; 4 radix passes over 32-bit keys."""
     V, C, P = st["visible"], st["candidates"], st["pairs"]
     sh_b = 12 * (deg + 1) ** 2
-    passes = (24 + 13 + 7) // 8
     return {
-        "preprocess": 48 * n + 4 * n + V * (sh_b + 80 + 112 + 16),
+        # geometry 48 B/Gaussian + count write; per visible: SH read, cull record 128 B, raster
+        # record 112 B and colour 16 B written
+        "preprocess": 48 * n + 4 * n + V * (sh_b + 128 + 112 + 16),
         "scan": 8 * n,
-        "cull_emit": 80 * V + 4 * C + 12 * P,
-        "sort": 8 * P + 24 * passes * P,
-        "ranges": 8 * P,
-        "raster": 12 * P + 112 * P,
+        # cull record read once per visible Gaussian + its offset; (key, value) written per kept pair
+        "cull_emit": (128 + 4) * V + 8 * P,
+        # histogram pass reads the keys; 4 onesweep passes read and write (key, value)
+        "sort": 4 * P + 4 * 16 * P,
+        "ranges": 4 * P,
+        # K6: (key, value) of every list entry + its 112-B raster record; RGB written per pixel
+        "raster": 8 * P + 112 * P + 12 * px,
     }
+
+
+def init_dist(world, local):
+    import torch
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    backend = "single"
+    if world > 1:
+        import torch.distributed as dist
+        backend = os.environ.get("AAA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev, local, backend
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, dev):
+    import torch
+    if world <= 1:
+        return float(x)
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.to(dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed(fn, steps, stream, world, local, dev):
+    """W/K protocol: barrier + synchronize on both sides, CUDA events on the launching stream,
+    max over ranks; nvidia-smi clocks sampled during the region."""
+    import torch
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(e0.elapsed_time(e1), world, dev), clk.summary()
 
 
 def cpu_baseline(scene, cams, idx, budget_s=20.0):
@@ -169,7 +260,9 @@ def run_reference(args, world, rank):
     if rank != 0:
         return 0
     import oracle as O
-    scene, cams, idx = scene_and_views(args.config, 0, 1, args.views_per_rank)
+    from synth import scenes as S
+    scene, cams = S.make_config(args.config)
+    idx = list(range(0, len(cams), max(1, len(cams) // 25)))[:25]
     O.build()
     orc = O.Oracle(scene)
     cores = O.num_threads()
@@ -205,11 +298,11 @@ def run_reference(args, world, rank):
     frame_s = tp / args.steps + tpx * (cam.width * cam.height) / npx
     v = 1.0 / frame_s
     sample = (f"per step: per-Gaussian stage on all {scene.n} Gaussians + {n_tiles} random 16x16 tiles "
-              f"({n_tiles * 256} px) of one c3 view; frames/s extrapolated to {cam.width}x{cam.height}")
+              f"({n_tiles * 256} px) of one {args.config} view; frames/s extrapolated to {cam.width}x{cam.height}")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": f"{args.config}: 3M Gaussians SH3 1920x1080, 200-view orbit",
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": workload_name(args, scene.n, cam.width, cam.height),
                                            "sample": sample},
            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -217,41 +310,111 @@ def run_reference(args, world, rank):
     return 0
 
 
+def workload_name(args, n, W, H):
+    if args.config == "c5":
+        return f"c5: {n / 1e6:g}M Gaussians SH3, one {W}x{H} frame split by cost-balanced tile-row bands"
+    if args.scaling == "strong":
+        return f"{args.config}: {n / 1e6:g}M Gaussians SH3, {W}x{H}, fixed {args.views}-view batch sharded by view"
+    return f"{args.config}: {n / 1e6:g}M Gaussians SH3, {W}x{H}, {args.views_per_rank} views per rank per step"
+
+
+def roofline_and_stages(R, views, n, deg, st_timed, abl, pkg):
+    """Per-stage algorithmic GB/s and the dominant kernel's roofline (K6: FP32 ALU)."""
+    R.set_config(flags=abl)
+    samp = []
+    for v in views[:: max(1, len(views) // 5)][:5]:
+        R.render(v, with_T=False)
+        samp.append(R.stats())
+    mean = {k: float(np.mean([s[k] for s in samp])) for k in
+            ("visible", "candidates", "pairs", "evaluations", "spilled_pixels", "deep_pixels",
+             "unresolved_pixels", "crossing")}
+    peaks, peaks_src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    fp32, fp32_src = fp32_peak()
+    px = views[0].width * views[0].height
+    stage_ms = dict(zip(STAGES, st_timed["ms"]))
+    sb = stage_bytes(mean, n, deg, px)
+    stages = {}
+    for k in STAGES[:7] + ["sync_gap"]:
+        t = stage_ms[k]
+        ent = {"ms_per_view": t, "share": t / stage_ms["total"] if stage_ms["total"] else None}
+        if k == "raster":
+            fl = mean["evaluations"] * EVAL_FLOPS  # evaluations counted in K6 only
+            ent.update(bound="alu", algo_bytes=sb[k], achieved_tflops=fl / (t * 1e-3) / 1e12 if t else None,
+                       frac_fp32=fl / (t * 1e-3) / 1e12 / fp32 if t else None,
+                       achieved_gbs=sb[k] / (t * 1e-3) / 1e9 if t else None)
+        elif k == "raster_spill":
+            ent.update(bound="alu/latency", note="K6s + K6d: the spilled pixels' remaining lists")
+        elif k == "cull_emit":
+            ent.update(bound="alu", algo_bytes=sb[k], achieved_gbs=sb[k] / (t * 1e-3) / 1e9 if t else None,
+                       note="FP32 box-minimum test + FP64 guard band: ALU/latency-bound, bytes for reference")
+        elif k in sb:
+            ent.update(bound="hbm", algo_bytes=sb[k], achieved_gbs=sb[k] / (t * 1e-3) / 1e9 if t else None,
+                       frac_hbm=sb[k] / (t * 1e-3) / 1e9 / hbm if t else None)
+        stages[k] = ent
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("raster_k6")
+        except Exception:
+            traffic = None
+    ach = stages["raster"]["achieved_tflops"]
+    roof = {"kernel": "raster (K6 k_raster)", "bound": "alu", "achieved": ach, "peak": fp32, "unit": "TFLOP/s",
+            "frac": ach / fp32 if ach else None, "traffic": traffic, "peak_source": fp32_src,
+            "work": f"{EVAL_FLOPS} FP32 ops x {mean['evaluations']:.4g} pixel-Gaussian evaluations per view (K6)",
+            "algo_bytes_per_view": sb["raster"]}
+    tot_b = sum(sb.values())
+    frame = {"algo_bytes_per_view": tot_b, "ms_per_view": stage_ms["total"],
+             "achieved_gbs": tot_b / (stage_ms["total"] * 1e-3) / 1e9 if stage_ms["total"] else None,
+             "peak_gbs": hbm, "peak_source": f"{peaks_src} hbm_gbs (MEASURED_PEAKS.json)"}
+    frame["frac"] = frame["achieved_gbs"] / hbm if frame["achieved_gbs"] else None
+    return roof, stages, mean, frame
+
+
 def run_ours(args, world, rank, local):
     import torch
     import paper_2504_12811_b200 as pkg
     from paper_2504_12811_b200 import _build
-
-    _build.build()
-    # one process per GPU; with fewer GPUs than ranks (a functional test of the N > 1 path on one
-    # device), ranks share devices round-robin and AAA_DIST_BACKEND=gloo avoids NCCL's one-rank-
-    # per-GPU rule
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        backend = os.environ.get("AAA_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
     from paper_2504_12811_b200 import partition as part
 
-    # rank 0 builds the scene; NCCL broadcasts it (the only pre-render collective)
+    _build.build()
+    dev, local, backend = init_dist(world, local)
+    # rank 0 builds the scene; NCCL broadcasts it (the only pre-render collective, SURVEY 8(e))
     scene_t, cams, sh_deg = part.load_scene_broadcast(args.config, rank, world, dev)
-    idx = part.view_block(len(cams), rank, world, args.views_per_rank)
-    views = [cams[i] for i in idx]
     R = pkg.Renderer(local)
     R.load(tensors=scene_t)
     n = int(scene_t["means"].shape[0])
     del scene_t
     torch.cuda.empty_cache()
-    H, W = views[0].height, views[0].width
-    out = torch.empty((len(views), 3, H, W), dtype=torch.float32, device=dev)
     abl = {"none": 0, "no_cull": pkg.AAA_FLAG_NO_TILE_CULL, "no_hier": pkg.AAA_FLAG_NO_HIER_SORT,
            "no_3d": pkg.AAA_FLAG_NO_3D}[args.ablation]
     R.set_config(flags=pkg.AAA_FLAG_TIMING | abl, window_k=int(os.environ.get("AAA_WINDOW_K", "32")))
+    stream = torch.cuda.current_stream(dev)
+    if args.config == "c5":
+        res = bands_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n)
+    else:
+        res = views_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n, sh_deg, abl)
+    if rank == 0:
+        res.update({"n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                    "vs_baseline": None, "dtype": "f32",
+                    "data": f"synthetic (seeded {args.config} generator; no datasets or trained weights exist offline)",
+                    "context": PAPER_CONTEXT, "dist_backend": backend})
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def views_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n, sh_deg, abl):
+    import torch
+    if args.scaling == "strong":
+        idx = part.view_shard(min(args.views, len(cams)), rank, world)
+    else:
+        idx = part.view_block(len(cams), rank, world, args.views_per_rank)
+    views = [cams[i] for i in idx]
+    H, W = views[0].height, views[0].width
+    out = torch.empty((len(views), 3, H, W), dtype=torch.float32, device=dev)
 
     def step():
         R.render_batch(views, out_rgb=out)
@@ -261,101 +424,54 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     R.stats()                      # reset the timing accumulation
     launches0 = R.stats()["launches"]
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    ms = e0.elapsed_time(e1)
+    ms_max, clocks = timed(step, args.steps, stream, world, local, dev)
     st_timed = R.stats()
     launches = st_timed["launches"] - launches0
-    ms_t = torch.tensor([ms], device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    total_views = args.steps * len(views) * world
+    total_views = args.steps * (min(args.views, len(cams)) if args.scaling == "strong" else len(views) * world)
     value = total_views / (ms_max / 1000.0)
 
-    # per-view counters (V, C, P, E) on a sample of this rank's views, timing off
-    R.set_config(flags=abl)
-    samp = []
-    for v in views[:: max(1, len(views) // 5)]:
-        R.render(v, with_T=False)
-        samp.append(R.stats())
-    mean = {k: float(np.mean([s[k] for s in samp])) for k in
-            ("visible", "candidates", "pairs", "evaluations", "spilled_pixels", "unresolved_pixels",
-             "crossing")}
-    peaks, peaks_src = measured_peaks()
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    stage_ms = dict(zip(STAGES, st_timed["ms"]))
-    sb = stage_bytes(mean, n, 3)
-    stages = {}
-    for k in STAGES[:7] + ["sync_gap"]:
-        t = stage_ms[k]
-        ent = {"ms_per_view": t, "share": t / stage_ms["total"] if stage_ms["total"] else None}
-        if k == "raster":
-            # K6 + K6s (spilled-pixel continuation) form one raster unit
-            t_all = t + stage_ms["raster_spill"]
-            fl = mean["evaluations"] * EVAL_FLOPS
-            ent.update(bound="alu", ms_incl_fallback=t_all,
-                       achieved_tflops=fl / (t_all * 1e-3) / 1e12 if t_all else None,
-                       achieved_gbs=sb[k] / (t_all * 1e-3) / 1e9 if t_all else None)
-        elif k in sb:
-            ent.update(bound="hbm", algo_bytes=sb[k], achieved_gbs=sb[k] / (t * 1e-3) / 1e9 if t else None)
-        stages[k] = ent
-    unit_ms = {k: stage_ms[k] for k in STAGES[:5]}
-    unit_ms["raster"] = stage_ms["raster"] + stage_ms["raster_spill"]
-    dom = max(unit_ms, key=unit_ms.get)
-    traffic = None
-    tp = ROOT / "profiles" / "ncu_traffic.json"
-    if tp.exists():
-        try:
-            traffic = json.loads(tp.read_text()).get(dom)
-        except Exception:
-            traffic = None
-    if stages[dom]["bound"] == "alu":
-        ach = stages[dom]["achieved_tflops"]
-        roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)",
-                "work": f"{EVAL_FLOPS} FP32 ops x {mean['evaluations']:.3g} pixel-Gaussian evaluations per view"}
-    else:
-        ach = stages[dom]["achieved_gbs"]
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": traffic, "peak_source": f"{peaks_src} hbm_gbs (MEASURED_PEAKS.json)",
-                "work": f"{stages[dom]['algo_bytes']:.4g} algorithmic bytes per view"}
+    # the same steps followed by the NCCL gather of every image to rank 0 ("report with
+    # and without the gather")
+    gather = None
+    if world > 1 and not args.no_gather:
+        def step_g():
+            step()
+            part.gather_views(out, rank, world)
+        step_g()
+        ms_g, _ = timed(step_g, max(1, args.steps // 2), stream, world, local, dev)
+        steps_g = max(1, args.steps // 2)
+        gather = {"value_with_gather": total_views / args.steps * steps_g / (ms_g / 1000.0),
+                  "ms_per_step_with_gather": ms_g / steps_g,
+                  "gather_ms_per_step": ms_g / steps_g - ms_max / args.steps,
+                  "bytes_to_rank0_per_step": (world - 1) * len(views) * 3 * H * W * 4,
+                  "how": "torch.distributed.gather of each rank's f32 RGB images to rank 0 after every step"}
+
+    roof, stages, mean, frame = roofline_and_stages(R, views, n, sh_deg, st_timed, abl, pkg)
 
     # e2e: the public C-ABI with HOST output buffers; D2H of every rendered image inside the region
     e2e = None
     if not args.no_e2e:
-        host = torch.empty((len(views), 3, H, W), dtype=torch.float32, pin_memory=True)
+        chunk = min(25, len(views))
+        host = torch.empty((chunk, 3, H, W), dtype=torch.float32, pin_memory=True)
         ptr = host.data_ptr()
-        R.render_batch(views, host_ptrs=(ptr, 0))
-        if world > 1:
-            torch.distributed.barrier()
-        t0 = time.perf_counter()
+
+        def step_e2e():
+            for c0 in range(0, len(views), chunk):
+                R.render_batch(views[c0:c0 + chunk], host_ptrs=(ptr, 0))
+
+        step_e2e()
+        barrier(world)
         n_e2e = max(1, args.steps // 2)
+        t0 = time.perf_counter()
         for _ in range(n_e2e):
-            R.render_batch(views, host_ptrs=(ptr, 0))
+            step_e2e()
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        dt_t = torch.tensor([dt], device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(dt_t, op=torch.distributed.ReduceOp.MAX)
-        ev = n_e2e * len(views) * world / float(dt_t.item())
-        e2e = {"value": ev, "unit": "frames/s", "h2d_bytes_per_step": len(views) * 88,
-               "d2h_bytes_per_step": len(views) * 3 * H * W * 4,
-               "how": "aaa_render_batch with pinned host rgb buffers (library copies each image back); "
-                      "camera structs are the per-step input; wall clock, max over ranks"}
+        dt = max_over_ranks(time.perf_counter() - t0, world, dev)
+        e2e = {"value": total_views / args.steps * n_e2e / dt, "unit": "frames/s",
+               "h2d_bytes_per_step": len(views) * 88, "d2h_bytes_per_step": len(views) * 3 * H * W * 4,
+               "how": f"aaa_render_batch with pinned host rgb buffers ({chunk}-view ring; the library copies "
+                      "each image back, overlapped with the next view); camera structs are the per-step "
+                      "input; wall clock, max over ranks"}
         del host
 
     cpu = None
@@ -363,27 +479,89 @@ def run_ours(args, world, rank, local):
         from synth import scenes as S2
         sc, cm = S2.make_config(args.config)
         cpu = cpu_baseline(sc, cm, idx, budget_s=args.cpu_budget)
+    return {"metric": METRIC, "value": value, "unit": "frames/s", "ms_per_step": ms_max / args.steps,
+            "scaling": args.scaling,
+            "config": {"workload": workload_name(args, n, W, H), "views_per_step": total_views // args.steps,
+                       "views_per_rank_per_step": len(views), "ablation": args.ablation, "gaussians": n,
+                       "width": W, "height": H, "parallelism": f"view-sharded x{world}",
+                       "l2": (f"inputs larger than L2 ({n * 240 / 1e6:.0f} MB scene re-streamed per view), no flush"
+                              if n * 240 > 126e6 else
+                              f"scene ({n * 240 / 1e6:.0f} MB) fits in L2 and stays resident across views, no flush")},
+            "mpix_per_s": value * W * H / 1e6, "roofline": roof, "frame_hbm": frame, "stages": stages,
+            "counters_per_view": mean, "gather": gather, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks}
 
-    if rank == 0:
-        res = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-               "data": f"synthetic (seeded {args.config} generator; no datasets or trained weights exist offline)",
-               "config": {"workload": f"{args.config}: {n / 1e6:g}M Gaussians SH{sh_deg}, {W}x{H}, "
-                                      f"{len(cams)}-view set; {len(views)} views per rank per step",
-                          "views_per_rank_per_step": len(views), "ablation": args.ablation, "gaussians": n, "width": W, "height": H,
-                          "parallelism": f"view-sharded x{world}",
-                          "l2": (f"inputs larger than L2 ({n * 240 / 1e6:.0f} MB scene re-streamed per view), no flush"
-                                 if n * 240 > 126e6 else
-                                 f"scene ({n * 240 / 1e6:.0f} MB) fits in L2 and stays resident across views, no flush")},
-               "mpix_per_s": value * W * H / 1e6,
-               "roofline": roof, "stages": stages, "counters_per_view": mean,
-               "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-               "clocks": clk.summary(), "context": PAPER_CONTEXT}
-        print(json.dumps(res), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
-    return 0
+
+def bands_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n):
+    """c5: one 4K frame per step split by cost-balanced tile-row bands (aaa_render_band: K1
+    replicated, K2-K6 on this rank's band); the NCCL band gather is timed separately."""
+    import torch
+    cam = cams[0]
+    H, W = cam.height, cam.width
+    R.set_camera(cam)
+    buf = torch.empty((3 * H * W,), dtype=torch.float32, device=dev)
+    state = {}
+
+    def step():
+        rgb, _, cuts = R.render_band(rank, world, out_rgb=buf)
+        state["rgb"], state["cuts"] = rgb, cuts
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    R.stats()
+    launches0 = R.stats()["launches"]
+    ms_max, clocks = timed(step, args.steps, stream, world, local, dev)
+    st_timed = R.stats()
+    launches = st_timed["launches"] - launches0
+    cuts = state["cuts"]
+    bands = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    value = args.steps / (ms_max / 1000.0)
+    gather = None
+    if world > 1 and not args.no_gather:
+        def step_g():
+            step()
+            part.gather_bands(state["rgb"], bands, W, H, rank, world)
+        step_g()
+        steps_g = max(1, args.steps // 2)
+        ms_g, _ = timed(step_g, steps_g, stream, world, local, dev)
+        gather = {"value_with_gather": steps_g / (ms_g / 1000.0), "ms_per_frame_with_gather": ms_g / steps_g,
+                  "gather_ms_per_frame": ms_g / steps_g - ms_max / args.steps,
+                  "how": "one NCCL all_gather_into_tensor of equal-size padded bands (partition.gather_bands)"}
+    # e2e: the frame on rank 0's host — band render, device gather, D2H of the whole frame
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((3, H, W), dtype=torch.float32, pin_memory=True)
+
+        def step_e2e():
+            step()
+            frame = part.gather_bands(state["rgb"], bands, W, H, rank, world) if world > 1 else state["rgb"]
+            if rank == 0:
+                host.copy_(frame, non_blocking=True)
+            torch.cuda.synchronize()
+
+        step_e2e()
+        barrier(world)
+        n_e2e = max(1, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            step_e2e()
+        dt = max_over_ranks(time.perf_counter() - t0, world, dev)
+        e2e = {"value": n_e2e / dt, "unit": "frames/s", "h2d_bytes_per_step": 88,
+               "d2h_bytes_per_step": 3 * H * W * 4,
+               "how": "aaa_render_band per rank + band gather + D2H of the full frame to rank 0's pinned host "
+                      "buffer; wall clock, max over ranks"}
+    st = R.stats()
+    stage_ms = dict(zip(STAGES, st_timed["ms"]))
+    return {"metric": "frames/s (6M-Gaussian SH3 3840x2160 frame, tile-row bands)", "value": value,
+            "unit": "frames/s", "ms_per_step": ms_max / args.steps, "ms_per_frame": ms_max / args.steps,
+            "scaling": "strong",
+            "config": {"workload": workload_name(args, n, W, H), "gaussians": n, "width": W, "height": H,
+                       "parallelism": f"tile-row bands x{world}", "bands": bands,
+                       "l2": "inputs (1.44 GB scene) larger than L2, no flush"},
+            "mpix_per_s": value * W * H / 1e6, "stages_rank0": {k: stage_ms[k] for k in STAGES},
+            "counters_rank0_band": {k: st[k] for k in ("visible", "candidates", "pairs", "evaluations")},
+            "gather": gather, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None}
 
 
 def main():
@@ -392,14 +570,22 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3")
+    ap.add_argument("--config", default="c3", help="c2, c3 (default), c4wide, c4zoomout, c4inside, c5")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: a fixed --views batch sharded by view (default, the c3 config); "
+                         "weak: --views-per-rank views per rank")
+    ap.add_argument("--views", type=int, default=200)
     ap.add_argument("--views-per-rank", type=int, default=25)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ablation", default="none", choices=["none", "no_cull", "no_hier", "no_3d"],
                     help="Table 5 switches (P:521-524): no 3D tile culling / no per-pixel re-sort / 2D splats")
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, world, rank)

@@ -190,8 +190,21 @@ aaa_status aaa_render_tiles(aaa_ctx* ctx, int32_t tile_row_begin, int32_t tile_r
                             float* T_band);
 
 /* Per-tile-row candidate cost of the current camera (sum of candidate tiles of every visible
- * Gaussian on each tile row), used to balance tile bands; out: ceil(H/16) int64. Syncs. */
+ * Gaussian on each tile row), used to balance tile bands; out: host, ceil(H/16) int64. Runs K1
+ * and a device row histogram only. Syncs. */
 aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows);
+
+/* One frame split across `world` ranks by screen-space tile-row bands (the c5 partition of
+ * SURVEY 8(e); the paper itself renders on one GPU): K1 runs on every Gaussian for the whole
+ * frame (replicated on every rank), its per-row candidate costs (as aaa_tile_row_costs) cut the R
+ * tile rows into `world` contiguous bands of near-equal cost — the same cut on every rank, no
+ * communication — and K2-K6 run for this rank's band only. cuts (host, world + 1 int32, out): band
+ * r is tile rows [cuts[r], cuts[r+1]). rgb (device or host): capacity 3 x H x W floats; the band is
+ * written as 3 planes of band_h x W, band_h = min(16 cuts[rank+1], H) - 16 cuts[rank]; T (nullable):
+ * band_h x W. Output is bit-identical to the same rows of aaa_render.
+ * Errors: AAA_ERR_INVALID_ARG (world < 1, rank outside [0, world), world > R, null rgb/cuts),
+ * AAA_ERR_STATE (no scene or camera). Synchronises twice internally (row costs, pair count). */
+aaa_status aaa_render_band(aaa_ctx* ctx, int32_t rank, int32_t world, float* rgb, float* T, int32_t* cuts);
 
 /* Training sampling frequency v_hat_train (Eq. 6): for every loaded
  * Gaussian, the maximum over the cameras whose view frustum contains its mean of f / z, with z

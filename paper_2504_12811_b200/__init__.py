@@ -208,6 +208,24 @@ class Renderer:
                "aaa_render_tiles")
         return out_rgb, out_T
 
+    def render_band(self, rank: int, world: int, out_rgb=None, out_T=None):
+        """This rank's tile-row band of the current camera's frame split over `world` ranks
+        (aaa_render_band). Returns (rgb[3, band_h, W] view into out_rgb, T or None, cuts[world+1])."""
+        torch = self.torch
+        H, W = self.height, self.width
+        dev = torch.device("cuda", self.device)
+        if out_rgb is None:
+            out_rgb = torch.empty((3 * H * W,), dtype=torch.float32, device=dev)
+        cuts = np.zeros(world + 1, dtype=np.int32)
+        tp = C.c_void_p(out_T.data_ptr()) if out_T is not None else C.c_void_p()
+        _check(self._ctx, lib().aaa_render_band(self._ctx, int(rank), int(world), C.c_void_p(out_rgb.data_ptr()), tp,
+                                                cuts.ctypes.data_as(C.POINTER(C.c_int32))), "aaa_render_band")
+        a, b = int(cuts[rank]), int(cuts[rank + 1])
+        bh = min(16 * b, H) - 16 * a
+        rgb = out_rgb.reshape(-1)[: 3 * bh * W].view(3, bh, W)
+        T = out_T.reshape(-1)[: bh * W].view(bh, W) if out_T is not None else None
+        return rgb, T, cuts
+
     def tile_row_costs(self) -> np.ndarray:
         rows = (self.height + 15) // 16
         out = np.zeros(rows, dtype=np.int64)

@@ -18,7 +18,8 @@ AAA_DBG_GAUSS_FIELDS = 26
 EXPORTED_SYMBOLS = ["aaa_version", "aaa_create", "aaa_destroy", "aaa_set_stream", "aaa_default_config",
                     "aaa_set_config", "aaa_load_gaussians", "aaa_set_camera", "aaa_render", "aaa_render_batch",
                     "aaa_render_tiles", "aaa_tile_row_costs", "aaa_get_stats", "aaa_synchronize",
-                    "aaa_debug_copy", "aaa_last_error", "aaa_compute_vtrain", "aaa_render_backward"]
+                    "aaa_debug_copy", "aaa_last_error", "aaa_compute_vtrain", "aaa_render_backward",
+                    "aaa_render_band"]
 
 
 class AaaError(RuntimeError):
@@ -78,6 +79,7 @@ def lib(path: Path | None = None):
         L.aaa_render_batch.argtypes = [V, C.POINTER(Camera), I32, V, V]
         L.aaa_render_tiles.argtypes = [V, I32, I32, V, V]
         L.aaa_tile_row_costs.argtypes = [V, C.POINTER(I64), I32]
+        L.aaa_render_band.argtypes = [V, I32, I32, V, V, C.POINTER(I32)]
         L.aaa_get_stats.argtypes = [V, C.POINTER(Stats)]
         L.aaa_synchronize.argtypes = [V]
         L.aaa_debug_copy.argtypes = [V, I32, V, C.c_size_t, C.POINTER(C.c_size_t)]

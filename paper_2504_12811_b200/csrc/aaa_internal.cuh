@@ -2,6 +2,7 @@
 // B200 forward renderer. See DESIGN.md "Data layout in HBM" for sizes.
 #pragma once
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "../../include/aaa.h"
@@ -75,6 +76,11 @@ struct __align__(16) CullRec {
     int32_t cross_slot;             // >= 0: index into CrossRec (exact QP path); -1 otherwise
     uint32_t zkey;                  // log-depth code of the depth lower bound (reading 23)
 };
+// the tile rect read as one 16-byte word (x = tx0 | ty0 << 16, y = tx1 | ty1 << 16)
+constexpr int CULLREC_RECT_U4 = 6;
+static_assert(offsetof(CullRec, tx0) == 16 * CULLREC_RECT_U4 && offsetof(CullRec, tx1) == 16 * CULLREC_RECT_U4 + 4,
+              "CullRec rect layout");
+static_assert(sizeof(CullRec) == 128, "CullRec is 128 B");
 
 // Gaussians whose tau-ellipsoid reaches z <= near: the exact QP culling path needs T_view.
 struct CrossRec {
@@ -199,6 +205,8 @@ void launch_aabb(const SceneDev& sc, float* d_blk, cudaStream_t st);
 void launch_permute(const float4* in, float4* out, const uint32_t* perm, int64_t n, int chunks, cudaStream_t st);
 void launch_vtrain(const SceneDev& sc, const VtCam* cams, int n_cams, float* out, bool store, cudaStream_t st);
 void launch_raster_fallback(const ViewParams& vp, const RasterArgs& ra, cudaStream_t st);
+void launch_row_costs(const ViewBufs& vb, int64_t n, int rows, unsigned long long* diff, cudaStream_t st);
+void launch_band_clip(const ViewBufs& vb, int64_t n, int row_begin, int row_end, cudaStream_t st);
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set it once per (kernel, device, size)
 // for the current device (thread-safe); a failure is returned and also left in cudaGetLastError()
 // for the launching entry point to report.

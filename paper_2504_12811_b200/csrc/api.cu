@@ -95,6 +95,10 @@ struct aaa_ctx {
     bool saved = false;     // rec holds the render of slot `cur`
     float* bwd_acc = nullptr;
     size_t bwd_acc_cap = 0;
+    // tile-band cost model (aaa_render_band / aaa_tile_row_costs): device row difference array
+    unsigned long long* d_rowdiff = nullptr;
+    unsigned long long* h_rowdiff = nullptr;  // pinned
+    int rowdiff_cap = 0;
     uint32_t* bwd_overflow = nullptr;
 };
 
@@ -322,11 +326,60 @@ aaa_status ensure_out(aaa_ctx* ctx, Slot& sl, size_t floats) {
     return AAA_OK;
 }
 
+aaa_status ensure_rowdiff(aaa_ctx* ctx, int rows) {
+    if (rows + 1 <= ctx->rowdiff_cap) return AAA_OK;
+    cudaFree(ctx->d_rowdiff);
+    cudaFreeHost(ctx->h_rowdiff);
+    ctx->d_rowdiff = nullptr;
+    ctx->h_rowdiff = nullptr;
+    ctx->rowdiff_cap = 0;
+    CU(cudaMalloc(&ctx->d_rowdiff, (size_t)(rows + 1) * sizeof(unsigned long long)));
+    CU(cudaMallocHost(&ctx->h_rowdiff, (size_t)(rows + 1) * sizeof(unsigned long long)));
+    ctx->rowdiff_cap = rows + 1;
+    return AAA_OK;
+}
+
+// per-row candidate costs of the slot's full-frame K1 (device histogram, one small D2H; syncs ps)
+aaa_status row_costs(aaa_ctx* ctx, const Slot& sl, int rows, cudaStream_t ps, std::vector<int64_t>& out) {
+    aaa_status s = ensure_rowdiff(ctx, rows);
+    if (s) return s;
+    launch_row_costs(sl.vb, ctx->scene.n, rows, ctx->d_rowdiff, ps);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(ctx->h_rowdiff, ctx->d_rowdiff, (size_t)(rows + 1) * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, ps));
+    CU(cudaStreamSynchronize(ps));
+    out.assign(rows, 0);
+    int64_t acc = 0;
+    for (int r = 0; r < rows; r++) {
+        acc += (int64_t)ctx->h_rowdiff[r];
+        out[r] = acc;
+    }
+    return AAA_OK;
+}
+
+// contiguous bands of near-equal cost: cut k is the first row whose cost prefix reaches k/world of
+// the total (every row also counts 1e-9, so empty rows still split), each band >= 1 row
+void split_bands(const std::vector<int64_t>& cost, int world, int32_t* cuts) {
+    const int R = (int)cost.size();
+    std::vector<double> pref(R + 1, 0.0);
+    for (int r = 0; r < R; r++) pref[r + 1] = pref[r] + (double)cost[r] + 1e-9;
+    cuts[0] = 0;
+    for (int k = 1; k < world; k++) {
+        const double target = pref[R] * k / world;
+        const int r = (int)(std::lower_bound(pref.begin(), pref.end(), target) - pref.begin());
+        cuts[k] = std::min(std::max(r, cuts[k - 1] + 1), R - (world - k));
+    }
+    cuts[world] = R;
+}
+
 // Run the pipeline for one view in slot ctx->cur into device buffers rgb (3 x out_h x W) / T
 // (nullptr = the slot's staging image, copied to host_rgb / host_T on the raster stream).
 // stop_after: 1 = after K3 (unsorted pairs kept, nothing on the raster stream), 0 = full render.
+// band_world > 0: tile-band mode (aaa_render_band): K1 for the whole frame, then this rank's band
+// of the cost-balanced split (cuts written to band_cuts).
 aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_end, float* rgb, float* T,
-                    float* host_rgb, float* host_T, bool debug_k1, int stop_after) {
+                    float* host_rgb, float* host_T, bool debug_k1, int stop_after, int band_rank = -1,
+                    int band_world = 0, int32_t* band_cuts = nullptr) {
     Slot& sl = ctx->slot[ctx->cur];
     cudaStream_t ps = ctx->pstream, rs = ctx->rstream;
     const int64_t n = ctx->scene.n;
@@ -358,6 +411,18 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     CU(cudaMemsetAsync(sl.vb.scan_state, 0, s2 * sizeof(uint32_t), ps));
     mark(0, ps);
     launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
+    if (band_world > 0) {
+        std::vector<int64_t> cost;
+        s = row_costs(ctx, sl, vp.tiles_y, ps, cost);
+        if (s) return s;
+        split_bands(cost, band_world, band_cuts);
+        row_begin = band_cuts[band_rank];
+        row_end = band_cuts[band_rank + 1];
+        vp.tile_row_begin = row_begin;
+        vp.tile_row_end = row_end;
+        launch_band_clip(sl.vb, n, row_begin, row_end, ps);
+        if (n > 0) ctx->launches += 2;
+    }
     mark(1, ps);
     if (n > 0) ctx->launches += 2;
     launch_scan(sl.vb.counts, sl.vb.offsets, n, &sl.vb.counters[CNT_C], sl.vb.scan_state,
@@ -501,7 +566,7 @@ aaa_status sync_all(aaa_ctx* ctx) {
 }
 
 aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int row_begin, int row_end, float* rgb,
-                         float* T) {
+                         float* T, int band_rank = -1, int band_world = 0, int32_t* band_cuts = nullptr) {
     if (!ctx) return AAA_ERR_INVALID_ARG;
     if (!ctx->loaded) return fail(ctx, AAA_ERR_STATE, "render before aaa_load_gaussians");
     if (!rgb) return fail(ctx, AAA_ERR_INVALID_ARG, "rgb output is null");
@@ -516,11 +581,11 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
     if (row_begin < 0 || row_end > ty || row_begin >= row_end)
         return fail(ctx, AAA_ERR_INVALID_ARG, "tile row band out of range");
     const int out_h = std::min(row_end * TILE, H) - row_begin * TILE;
-    const size_t plane = (size_t)out_h * W;
+    size_t plane = (size_t)out_h * W;
     const bool dev_rgb = is_device_ptr(rgb);
     const bool dev_T = T ? is_device_ptr(T) : true;
     const bool save = (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) != 0;
-    if (save && (n_views != 1 || row_begin != 0 || row_end != ty ||
+    if (save && (n_views != 1 || row_begin != 0 || row_end != ty || band_world > 0 ||
                  (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))))
         return fail(ctx, AAA_ERR_INVALID_ARG, "AAA_FLAG_SAVE_CONTRIBS needs a single full-image default render");
     ctx->saved = false;
@@ -532,7 +597,7 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
         float* t = T && dev_T ? T + plane * v : nullptr;
         float* hr = dev_rgb ? nullptr : rgb + 3 * plane * v;
         float* ht = T && !dev_T ? T + plane * v : nullptr;
-        s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0);
+        s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0, band_rank, band_world, band_cuts);
     }
     if (save && !s) {
         // a pixel that blended more than rec_cap contributions: grow the record and render again
@@ -615,6 +680,8 @@ void aaa_destroy(aaa_ctx* ctx) {
     cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh); cudaFree(s.perm);
     for (auto& sl : ctx->slot) free_slot(sl);
     cudaFree(ctx->rec); cudaFree(ctx->rec_n); cudaFree(ctx->bwd_acc); cudaFree(ctx->bwd_overflow);
+    cudaFree(ctx->d_rowdiff);
+    if (ctx->h_rowdiff) cudaFreeHost(ctx->h_rowdiff);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev_pool)
         for (auto x : e) cudaEventDestroy(x);
@@ -827,18 +894,37 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
     if (!ctx->loaded || !ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "need scene and camera");
     const int ty = (ctx->cam.height + TILE - 1) / TILE;
     if (n_rows < ty) return fail(ctx, AAA_ERR_INVALID_ARG, "n_rows < tile rows");
-    SETDEV(ctx);
-    aaa_status s = run_debug_view(ctx, false);
+    aaa_status s = enter(ctx);
     if (s) return s;
-    const Slot& sl = ctx->slot[ctx->cur];
-    uint32_t P = 0;
-    CU(cudaMemcpy(&P, &sl.vb.counters[CNT_P], sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    std::vector<skey_t> keys(P);
-    if (P) CU(cudaMemcpy(keys.data(), sl.sb.keys[0], P * sizeof(skey_t), cudaMemcpyDeviceToHost));
-    const int tx = (ctx->cam.width + TILE - 1) / TILE;
-    for (int r = 0; r < n_rows; r++) out[r] = 0;
-    for (uint32_t i = 0; i < P; i++) out[(keys[i] >> sl.vp.key_db) / tx]++;
-    return AAA_OK;
+    ctx->cur ^= 1;
+    ctx->saved = false;
+    Slot& sl = ctx->slot[ctx->cur];
+    cudaStream_t ps = ctx->pstream;
+    CU(cudaStreamWaitEvent(ps, sl.raster_done, 0));
+    s = ensure_view_bufs(ctx, sl, ctx->scene.n);
+    if (s) return s;
+    ViewParams vp = make_view(ctx, ctx->cam, 0, ty);
+    CU(cudaMemsetAsync(sl.vb.counters, 0, CNT_TOTAL * sizeof(uint32_t), ps));
+    launch_preprocess(ctx->scene, vp, sl.vb, false, ps);
+    sl.vp = vp;
+    std::vector<int64_t> cost;
+    s = row_costs(ctx, sl, ty, ps, cost);
+    if (s) return s;
+    CU(cudaEventRecord(sl.raster_done, ps));
+    for (int r = 0; r < n_rows; r++) out[r] = r < ty ? cost[r] : 0;
+    s = leave(ctx);
+    if (s) return s;
+    return sync_all(ctx);
+}
+
+aaa_status aaa_render_band(aaa_ctx* ctx, int32_t rank, int32_t world, float* rgb, float* T, int32_t* cuts) {
+    if (!ctx) return AAA_ERR_INVALID_ARG;
+    if (!ctx->have_cam) return fail(ctx, AAA_ERR_STATE, "render before aaa_set_camera");
+    if (!cuts) return fail(ctx, AAA_ERR_INVALID_ARG, "cuts is null");
+    const int ty = (ctx->cam.height + TILE - 1) / TILE;
+    if (world < 1 || rank < 0 || rank >= world || world > ty)
+        return fail(ctx, AAA_ERR_INVALID_ARG, "need 1 <= world <= tile rows and 0 <= rank < world");
+    return render_common(ctx, &ctx->cam, 1, 0, ty, rgb, T, rank, world, cuts);
 }
 
 aaa_status aaa_compute_vtrain(aaa_ctx* ctx, const aaa_camera* cams, int32_t n_cams, float* out, int32_t store) {

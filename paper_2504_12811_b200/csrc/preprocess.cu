@@ -603,4 +603,65 @@ void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, b
         k_preprocess<false><<<blocks, threads, 0, st>>>(sc, vp, vb);
 }
 
+// Tile-band cost model: per tile row, the number of candidate (Gaussian, rect
+// tile) pairs of a full-frame K1 — identical on every rank, so every rank derives the same bands
+// without communication. Difference array over rows (+w at ty0, -w at ty1 + 1, w = rect width),
+// accumulated per block in shared memory and flushed with one 64-bit atomic per row per block.
+constexpr int ROWCOST_SMEM_ROWS = 2048;
+__global__ void __launch_bounds__(256) k_row_costs(const CullRec* __restrict__ cull, const uint32_t* __restrict__ counts,
+                                                   int64_t n, int rows, unsigned long long* diff) {
+    __shared__ int32_t h[ROWCOST_SMEM_ROWS + 1];
+    const bool sm = rows <= ROWCOST_SMEM_ROWS;
+    if (sm)
+        for (int i = threadIdx.x; i <= rows; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
+        if (counts[g] == 0) continue;
+        const uint4 rr = reinterpret_cast<const uint4*>(cull + g)[CULLREC_RECT_U4];
+        const int tx0 = rr.x & 0xFFFF, ty0 = rr.x >> 16, tx1 = rr.y & 0xFFFF, ty1 = rr.y >> 16;
+        const int w = tx1 - tx0 + 1;
+        if (sm) {
+            atomicAdd(&h[ty0], w);
+            atomicAdd(&h[ty1 + 1], -w);
+        } else {
+            atomicAdd(&diff[ty0], (unsigned long long)(long long)w);
+            atomicAdd(&diff[ty1 + 1], (unsigned long long)(long long)(-w));
+        }
+    }
+    __syncthreads();
+    if (sm)
+        for (int i = threadIdx.x; i <= rows; i += blockDim.x)
+            if (h[i]) atomicAdd(&diff[i], (unsigned long long)(long long)h[i]);
+}
+
+// clip every visible Gaussian's tile rect to the band [row_begin, row_end) and recount its
+// candidates (after a full-frame K1): K2/K3 then emit only the band's pairs
+__global__ void __launch_bounds__(256) k_band_clip(CullRec* cull, uint32_t* counts, int64_t n, int row_begin,
+                                                   int row_end) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n || counts[g] == 0) return;
+    uint4* p = reinterpret_cast<uint4*>(cull + g) + CULLREC_RECT_U4;
+    uint4 rr = *p;
+    const int tx0 = rr.x & 0xFFFF, tx1 = rr.y & 0xFFFF;
+    const int ty0 = max((int)(rr.x >> 16), row_begin), ty1 = min((int)(rr.y >> 16), row_end - 1);
+    counts[g] = ty0 <= ty1 ? (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1) : 0u;
+    if (ty0 <= ty1) {
+        rr.x = (uint32_t)tx0 | ((uint32_t)ty0 << 16);
+        rr.y = (uint32_t)tx1 | ((uint32_t)ty1 << 16);
+        *p = rr;
+    }
+}
+
+void launch_row_costs(const ViewBufs& vb, int64_t n, int rows, unsigned long long* diff, cudaStream_t st) {
+    cudaMemsetAsync(diff, 0, (size_t)(rows + 1) * sizeof(unsigned long long), st);
+    if (n == 0) return;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_row_costs<<<blocks, 256, 0, st>>>(vb.cull, vb.counts, n, rows, diff);
+}
+
+void launch_band_clip(const ViewBufs& vb, int64_t n, int row_begin, int row_end, cudaStream_t st) {
+    if (n == 0) return;
+    k_band_clip<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vb.cull, vb.counts, n, row_begin, row_end);
+}
+
 }  // namespace aaa

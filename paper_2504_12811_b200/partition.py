@@ -47,6 +47,23 @@ def band_split(row_costs, world: int) -> list[tuple[int, int]]:
     return [(cuts[i], cuts[i + 1]) for i in range(world)]
 
 
+def _host_staged(t):
+    """gloo collectives run on host tensors (the N-ranks-on-fewer-GPUs functional mode and CPU
+    tests); NCCL ones on the device tensors themselves."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend() == "gloo"
+
+
+def _bcast(t, src):
+    import torch.distributed as dist
+    if _host_staged(t):
+        h = t.cpu()
+        dist.broadcast(h, src)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src)
+
+
 def scene_to_tensors(scene, device):
     import torch
     t = {f: torch.from_numpy(np.ascontiguousarray(getattr(scene, f), dtype=np.float32)).to(device)
@@ -67,7 +84,7 @@ def broadcast_scene(scene_or_none, rank: int, world: int, device, src: int = 0):
         meta = torch.tensor([t["means"].shape[0], t["sh_degree"]], dtype=torch.int64, device=device)
     else:
         meta = torch.zeros(2, dtype=torch.int64, device=device)
-    dist.broadcast(meta, src)
+    _bcast(meta, src)
     n, deg = int(meta[0]), int(meta[1])
     K = (deg + 1) ** 2
     shapes = {"means": (n, 3), "scales": (n, 3), "quats": (n, 4), "opacities": (n,), "sh": (n, K, 3),
@@ -76,7 +93,7 @@ def broadcast_scene(scene_or_none, rank: int, world: int, device, src: int = 0):
         t = {f: torch.empty(shapes[f], dtype=torch.float32, device=device) for f in SCENE_FIELDS}
         t["sh_degree"] = deg
     for f in SCENE_FIELDS:
-        dist.broadcast(t[f], src)
+        _bcast(t[f], src)
     return t
 
 
@@ -108,6 +125,20 @@ def _cameras_only(config: str):
     raise ValueError(config)
 
 
+def gather_views(images, rank: int, world: int, dst: int = 0):
+    """Gather every rank's rendered views (v_r x 3 x H x W, equal v_r on every rank) to `dst`:
+    one NCCL gather (rank `dst` receives world x v_r images). Returns the list on dst, else None."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return [images]
+    staged = _host_staged(images)
+    src = images.cpu() if staged else images
+    lst = [torch.empty_like(src) for _ in range(world)] if rank == dst else None
+    dist.gather(src, lst, dst=dst)
+    return lst
+
+
 def gather_bands(band_rgb, bands, width: int, height: int, rank: int, world: int, dst: int = 0):
     """Assemble tile-row bands (3 x band_h x W each) into the full 3 x H x W frame on `dst`
     with one NCCL all-gather of equal-size padded bands."""
@@ -117,7 +148,12 @@ def gather_bands(band_rgb, bands, width: int, height: int, rank: int, world: int
     pad = torch.zeros((3, max_h, width), dtype=band_rgb.dtype, device=band_rgb.device)
     pad[:, : band_rgb.shape[1]] = band_rgb
     out = torch.empty((world * 3, max_h, width), dtype=band_rgb.dtype, device=band_rgb.device)
-    dist.all_gather_into_tensor(out, pad)
+    if _host_staged(pad):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(h, pad.cpu())
+        out.copy_(h)
+    else:
+        dist.all_gather_into_tensor(out, pad)
     out = out.view(world, 3, max_h, width)
     if rank != dst:
         return None

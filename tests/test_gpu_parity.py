@@ -392,3 +392,31 @@ def test_invalid_inputs_rejected(R):
     R.load(one_gaussian((0, 0, 2.0), (0.1, 0.1, 0.1)))
     with pytest.raises(pkg.AaaError):
         R.set_camera(bad_cam)
+
+
+@pytest.mark.parametrize("cfg,world", [("c2", 3), ("c5", 8)])
+def test_render_band_equals_full_frame(R, cfg, world):
+    """aaa_render_band (SURVEY 8(e) tile bands): the bands of every rank, stacked, are the full
+    frame bit for bit; the cut is the cost-balanced split of aaa_tile_row_costs (partition.band_split
+    computes the same cut on the host)."""
+    from paper_2504_12811_b200 import partition as part
+    scene, cams = S.make_config(cfg)
+    cam = cams[11 if cfg == "c2" else 0]
+    R.load(scene)
+    full = _img(R, cam)
+    C_full = R.stats()["candidates"]
+    R.set_camera(cam)
+    costs = R.tile_row_costs()
+    assert costs.sum() == C_full
+    want_cuts = part.band_split(costs, world)
+    rows, cuts0 = [], None
+    for rank in range(world):
+        rgb, T, cuts = R.render_band(rank, world, out_T=torch.empty((cam.height * cam.width,), device="cuda:0"))
+        torch.cuda.synchronize()
+        if cuts0 is None:
+            cuts0 = cuts.copy()
+        assert np.array_equal(cuts, cuts0)
+        rows.append(torch.cat([rgb, T[None]], 0).permute(1, 2, 0).cpu().numpy())
+    assert [(int(a), int(b)) for a, b in zip(cuts0[:-1], cuts0[1:])] == want_cuts
+    got = np.concatenate(rows, axis=0).astype(np.float64)
+    assert np.array_equal(got, full)

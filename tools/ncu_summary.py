@@ -36,6 +36,18 @@ FULL_METRICS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads / instruction"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe % (active)"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe % (active)"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe % (active)"),
+    ("sm__inst_executed_pipe_fma.sum", "FMA-pipe warp instr"),
+    ("sm__inst_executed_pipe_alu.sum", "ALU-pipe warp instr"),
+    ("sm__inst_executed_pipe_xu.sum", "XU (MUFU) warp instr"),
+    ("sm__inst_executed_pipe_lsu.sum", "LSU warp instr"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem ld bank conflicts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem st bank conflicts"),
+    ("smsp__warps_issue_stalled_long_scoreboard_per_warp_active.pct", "stall long scoreboard %"),
+    ("smsp__warps_issue_stalled_short_scoreboard_per_warp_active.pct", "stall short scoreboard %"),
+    ("smsp__warps_issue_stalled_wait_per_warp_active.pct", "stall wait %"),
     ("launch__registers_per_thread", "registers"),
     ("launch__shared_mem_per_block_dynamic", "dyn smem / CTA (B)"),
     ("launch__grid_size", "grid"),
@@ -68,7 +80,7 @@ def main():
     tot = sum(per_view.values())
     lines = [f"# {r}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
              "Command: `ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 "
-             "--warmup 3 --views-per-rank 4 --no-cpu-baseline --no-e2e` (c3: 3M Gaussians, 1920x1080). "
+             "--warmup 3 --scaling weak --views-per-rank 4 --no-cpu-baseline --no-e2e` (c3: 3M Gaussians, 1920x1080). "
              "Per-launch times are cold-cache and serialised; compare the SHARE of a view with bench.py's "
              "`stages`.", "",
              f"{len(rows)} launches ({sum(len(v) for v in load.values())} at scene load), {n_views} views.", "",
@@ -89,7 +101,7 @@ def main():
         kern.append((base(d["Kernel Name"]), d))
     lines = [f"# {r}: ncu --set full of one c3 view (every kernel, 2nd rendered view)", "",
              "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 14 "
-             "python bench.py --steps 1 --warmup 3 --views-per-rank 1 --no-cpu-baseline --no-e2e`. "
+             "python bench.py --steps 1 --warmup 3 --scaling weak --views-per-rank 1 --no-cpu-baseline --no-e2e` (plus the pipe / bank-conflict metrics). "
              "ncu flushes caches before each replay (cold L2).", "",
              "| metric | " + " | ".join(k for k, _ in kern) + " |", "|---|" + "---|" * len(kern)]
     for m, label in FULL_METRICS:
@@ -116,6 +128,8 @@ def main():
             if k in ks:
                 b += (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * scale
         traffic[st] = b
+    traffic["raster_k6"] = sum((float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * scale
+                               for k, d in kern if k == "k_raster")
     traffic["_source"] = f"profiles/{r}_full.md (dram__bytes_read.sum + dram__bytes_write.sum, one c3 view)"
     (PROF / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print((PROF / f"{r}_launches.md").read_text())
