@@ -95,12 +95,14 @@ typedef struct {
  * the call): 0 preprocess (K1), 1 scan (K2), 2 cull/emit (K3), 3 sort (K4), 4 ranges (K5),
  * 5 raster (K6), 6 spilled-pixel continuation (K6s), 7 host-sync gap after K2, 8 output copy
  * (host outputs only), 9 total. deep_pixels: spilled pixels whose pending set outgrew K6s's
- * 256 entries (finished by K6d with 2048). */
+ * 256 entries (finished by K6d with 2048). giant_pixels: pixels of tiles whose list exceeded the
+ * giant-list threshold, rendered one warp per pixel by K6s from the list start (counted in
+ * spilled_pixels too). */
 typedef struct {
     int64_t n, visible, candidates, pairs, spilled_pixels, unresolved_pixels, crossing;
     int64_t evaluations, launches, timed_views;
     float ms[10];
-    int64_t deep_pixels;
+    int64_t deep_pixels, giant_pixels;
 } aaa_stats;
 
 /* aaa_config.flags:
@@ -113,6 +115,9 @@ typedef struct {
  *                            (test of the second spill level; the image is unchanged)
  *   AAA_FLAG_CULL_FP64       K3 decides every tile / sub-tile test in FP64 (no FP32 guard-band
  *                            fast path; test of the guard band: the pairs are unchanged)
+ *   AAA_FLAG_FORCE_GIANT     every tile with a list of more than one entry takes the giant-list
+ *                            path (one warp per pixel in K6s from the list start; test of that
+ *                            path: the image is unchanged)
  *   AAA_FLAG_NO_HIER_SORT    Table 5 "w/o hier. sort": blend in the global per-Gaussian
  *                            order only — tile lists sorted by the view depth of the mean, no
  *                            per-pixel re-sort (the image changes where that order is not z*)
@@ -133,6 +138,7 @@ enum {
                                    * only; the call synchronises */
     , AAA_FLAG_FORCE_DEEP = 64u
     , AAA_FLAG_CULL_FP64 = 128u
+    , AAA_FLAG_FORCE_GIANT = 256u
 };
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */

@@ -49,7 +49,8 @@ def render(params: dict, scene, cam, k=0.3, alpha_max=0.99, T_eps=1e-4, bg=(0.0,
     V = torch.tensor([[_f32(v) for v in row] for row in np.asarray(cam.world_to_view, np.float64)], dtype=torch.float64)
     Rv, tv = V[:3, :3], V[:3, 3]
     fx, fy, cx, cy, near = _f32(cam.fx), _f32(cam.fy), _f32(cam.cx), _f32(cam.cy), _f32(cam.near)
-    cam_o = -Rv.T @ tv
+    Rvi = torch.linalg.inv(Rv)  # the given affine map's exact inverse (reading 37)
+    cam_o = -Rvi @ tv
     vt = torch.tensor(np.asarray(scene.v_train, np.float64))
     # R(q), q normalised (Eq. 3)
     qn = q / q.norm(dim=1, keepdim=True)
@@ -83,7 +84,7 @@ def render(params: dict, scene, cam, k=0.3, alpha_max=0.99, T_eps=1e-4, bg=(0.0,
     H, W = cam.height, cam.width
     yy, xx = torch.meshgrid(torch.arange(H, dtype=torch.float64), torch.arange(W, dtype=torch.float64), indexing="ij")
     r = torch.stack([(xx + 0.5 - cx) / fx, (yy + 0.5 - cy) / fy, torch.ones_like(xx)], -1).reshape(-1, 3)
-    v = r @ Rv  # world direction with view-z 1 (rows: Rv^T r)
+    v = r @ Rvi.T  # world direction with view-z 1 (rows: Rv^-1 r)
     mo = mu - cam_o
     Sv = torch.einsum("nij,pj->pni", Shinv, v)           # S^-1 v   (P,N,3)
     vSv = torch.einsum("pi,pni->pn", v, Sv)

@@ -63,7 +63,7 @@ struct orc_scene {
     std::vector<double> means, scales, quats, opac, sh, vtrain;
     orc_camera cam;
     orc_config cfg;
-    double Rv[3][3], tv[3], o[3];  // world->view rotation/translation, camera centre
+    double Rv[3][3], Rvi[3][3], tv[3], o[3];  // world->view rotation (and its inverse), translation, camera centre
     std::vector<Prepared> prep;
     bool have_view = false;
 };
@@ -255,7 +255,7 @@ struct Contrib {
 // World-space direction v of pixel centre p with view-z component 1 (reading 26).
 inline void pixel_dir(const orc_scene* s, double px, double py, double* v) {
     double r[3] = {(px - s->cam.cx) / s->cam.fx, (py - s->cam.cy) / s->cam.fy, 1.0};
-    for (int i = 0; i < 3; i++) v[i] = s->Rv[0][i] * r[0] + s->Rv[1][i] * r[1] + s->Rv[2][i] * r[2];
+    for (int i = 0; i < 3; i++) v[i] = s->Rvi[i][0] * r[0] + s->Rvi[i][1] * r[1] + s->Rvi[i][2] * r[2];
 }
 
 // Maximum-response point of Gaussian g along the ray o + t v, by explicit
@@ -537,8 +537,12 @@ int32_t orc_set_view(orc_scene* s, const orc_camera* cam, const orc_config* cfg)
         for (int j = 0; j < 3; j++) s->Rv[i][j] = cam->world_to_view[4 * i + j];
         s->tv[i] = cam->world_to_view[4 * i + 3];
     }
-    for (int i = 0; i < 3; i++)  // o = -Rv^T t
-        s->o[i] = -(s->Rv[0][i] * s->tv[0] + s->Rv[1][i] * s->tv[1] + s->Rv[2][i] * s->tv[2]);
+    // The camera is the affine map x_v = Rv x + t as given (reading 37): the camera centre
+    // and the world-space pixel rays use the exact inverse Rv^-1 (the float32 matrix is
+    // orthonormal only to ~1e-7; Rv^T in its place moves z* by ~1e-5 relative near the near plane)
+    inv3(s->Rv, s->Rvi);
+    for (int i = 0; i < 3; i++)  // o = -Rv^-1 t
+        s->o[i] = -(s->Rvi[i][0] * s->tv[0] + s->Rvi[i][1] * s->tv[1] + s->Rvi[i][2] * s->tv[2]);
     s->prep.assign(s->n, Prepared());
 #pragma omp parallel for schedule(static)
     for (int64_t g = 0; g < s->n; g++) prepare_one(s, g, s->prep[g]);

@@ -10,6 +10,7 @@ AAA_FLAG_TIMING, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_FORCE_FALLBACK, AAA_FLAG_NO_HIE
 AAA_FLAG_SAVE_CONTRIBS = 32
 AAA_FLAG_FORCE_DEEP = 64
 AAA_FLAG_CULL_FP64 = 128
+AAA_FLAG_FORCE_GIANT = 256
 AAA_WARN_UNRESOLVED = 1  # aaa_get_stats / aaa_synchronize: pixels left inexact (spill queue full)
 (AAA_DBG_GAUSS, AAA_DBG_KEYS, AAA_DBG_VALS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_VALS_UNSORTED, AAA_DBG_RANGES,
  AAA_DBG_SPILL, AAA_DBG_RASTER, AAA_DBG_COLOR) = range(9)
@@ -51,7 +52,7 @@ class Stats(C.Structure):
     _fields_ = [("n", C.c_int64), ("visible", C.c_int64), ("candidates", C.c_int64), ("pairs", C.c_int64),
                 ("spilled_pixels", C.c_int64), ("unresolved_pixels", C.c_int64), ("crossing", C.c_int64), ("evaluations", C.c_int64),
                 ("launches", C.c_int64), ("timed_views", C.c_int64), ("ms", C.c_float * 10),
-                ("deep_pixels", C.c_int64)]
+                ("deep_pixels", C.c_int64), ("giant_pixels", C.c_int64)]
 
 
 _lib = None

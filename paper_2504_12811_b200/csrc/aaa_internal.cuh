@@ -28,7 +28,8 @@ constexpr int64_t MAX_GAUSSIANS = 1ll << VAL_INDEX_BITS;
 struct ViewParams {
     double Rv[9];       // world->view rotation (row-major)
     double tv[3];       // world->view translation
-    double o[3];        // camera centre in world space, -Rv^T tv
+    double Rvi[9];      // Rv^-1 (row-major; the exact inverse of the given float32 matrix, reading 37)
+    double o[3];        // camera centre in world space, -Rv^-1 tv
     double fx, fy, cx, cy, near_z;
     int width, height;
     int tiles_x, tiles_y;
@@ -45,6 +46,7 @@ struct ViewParams {
     float key_near_f;      // near_lo rounded down (decode)
     double inv_fx, inv_fy; // 1/fx, 1/fy
     double key_zmul;       // (1 - ZKEY_PAD) / key_near (encode)
+    uint32_t giant_list;   // K6: tiles whose list is longer go pixel by pixel to K6s (0 = never)
 };
 
 // Scene residency (L0): structure of float4 arrays, 16-byte aligned.
@@ -113,7 +115,7 @@ struct ViewBufs {
 constexpr int AAA_SP_CAP_LVL1 = AAA_SP_CAP;
 constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_SPILL = 4, CNT_SPILL_TICKET = 5,
               CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
-              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_TOTAL = 40;
+              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_TOTAL = 40;
 
 // ---- launchers (each file implements its own) ----
 void launch_load_pack(const aaa_gaussians& in, const float* dmeans, const float* dscales, const float* dquats,

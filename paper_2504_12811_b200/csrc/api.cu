@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -171,14 +172,36 @@ aaa_status check_camera(aaa_ctx* ctx, const aaa_camera* c) {
     return AAA_OK;
 }
 
+// Tiles with a list longer than this are rendered pixel by pixel (one warp per pixel, K6s) instead
+// of by 8x4 sub-tile warps (K6): on giant lists (c4 zoom-out) a sub-tile warp's serial walk is the
+// kernel's critical path. AAA_GIANT_LIST overrides (0 = off).
+uint32_t giant_list_threshold() {
+    static const uint32_t v = [] {
+        const char* e = getenv("AAA_GIANT_LIST");
+        return e ? (uint32_t)strtoul(e, nullptr, 10) : 0u;
+    }();
+    return v;
+}
+
 ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int row_end) {
     ViewParams vp{};
     for (int i = 0; i < 3; i++) {
         for (int j = 0; j < 3; j++) vp.Rv[3 * i + j] = c.world_to_view[4 * i + j];
         vp.tv[i] = c.world_to_view[4 * i + 3];
     }
-    // orthonormalise nothing: the camera was validated; o = -Rv^T t
-    for (int i = 0; i < 3; i++) vp.o[i] = -(vp.Rv[i] * vp.tv[0] + vp.Rv[3 + i] * vp.tv[1] + vp.Rv[6 + i] * vp.tv[2]);
+    // The camera is the given affine map x_v = Rv x + t (reading 37). Its float32 rotation block is
+    // orthonormal only to ~1e-7, so the inverse (camera centre, world -> Gaussian-space ray
+    // directions) is the exact 3x3 inverse in FP64, not Rv^T: with |t| ~ 2 and near = 0.01 the
+    // transpose shortcut would move z* near the near plane by ~1e-5 relative.
+    {
+        const double* a = vp.Rv;
+        const double c00 = a[4] * a[8] - a[5] * a[7], c01 = a[5] * a[6] - a[3] * a[8], c02 = a[3] * a[7] - a[4] * a[6];
+        const double det = a[0] * c00 + a[1] * c01 + a[2] * c02, id = 1.0 / det;
+        vp.Rvi[0] = c00 * id; vp.Rvi[1] = (a[2] * a[7] - a[1] * a[8]) * id; vp.Rvi[2] = (a[1] * a[5] - a[2] * a[4]) * id;
+        vp.Rvi[3] = c01 * id; vp.Rvi[4] = (a[0] * a[8] - a[2] * a[6]) * id; vp.Rvi[5] = (a[2] * a[3] - a[0] * a[5]) * id;
+        vp.Rvi[6] = c02 * id; vp.Rvi[7] = (a[1] * a[6] - a[0] * a[7]) * id; vp.Rvi[8] = (a[0] * a[4] - a[1] * a[3]) * id;
+    }
+    for (int i = 0; i < 3; i++) vp.o[i] = -(vp.Rvi[3 * i] * vp.tv[0] + vp.Rvi[3 * i + 1] * vp.tv[1] + vp.Rvi[3 * i + 2] * vp.tv[2]);
     vp.fx = c.fx; vp.fy = c.fy; vp.cx = c.cx; vp.cy = c.cy; vp.near_z = c.near_z;
     vp.width = c.width; vp.height = c.height;
     vp.tiles_x = (c.width + TILE - 1) / TILE;
@@ -208,6 +231,7 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     vp.inv_fx = 1.0 / vp.fx;
     vp.inv_fy = 1.0 / vp.fy;
     vp.key_zmul = (1.0 - ZKEY_PAD) / vp.key_near;
+    vp.giant_list = (ctx->cfg.flags & AAA_FLAG_FORCE_GIANT) ? 1u : giant_list_threshold();
     return vp;
 }
 
@@ -1027,6 +1051,7 @@ aaa_status aaa_get_stats(aaa_ctx* ctx, aaa_stats* out) {
     out->unresolved_pixels = h[CNT_UNRESOLVED];
     out->crossing = h[CNT_CROSS];
     out->deep_pixels = h[CNT_DEEP];
+    out->giant_pixels = h[CNT_GIANT];
     out->evaluations = h[CNT_EVAL];
 #ifdef AAA_DEBUG_STATS
     {

@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(64) k_bwd_gaussians(SceneDev sc, ViewParams vp
         Amp = dsqrt(num / den);
     }
     const Dn oA = op * Amp;
-    // W = diag(1/sig) (R_v R)^T (row j = column j of R_v R over sig_j); c = -W mu_v
+    // W = diag(1/sig) R^T R_v^-1 (reading 37); c = -W mu_v
     auto addg = [&](const Dn& x, float u) {
         if (u != 0.f)
             for (int k = 0; k < ND; k++) grad[k] += (double)u * x.d[k];
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(64) k_bwd_gaussians(SceneDev sc, ViewParams vp
     for (int j = 0; j < 3; j++) {
         const Dn isg = 1.0 / sig[j];
         for (int i = 0; i < 3; i++) {
-            const Dn Qij = R[j] * vp.Rv[3 * i] + R[3 + j] * vp.Rv[3 * i + 1] + R[6 + j] * vp.Rv[3 * i + 2];
+            const Dn Qij = R[j] * vp.Rvi[i] + R[3 + j] * vp.Rvi[3 + i] + R[6 + j] * vp.Rvi[6 + i];
             W[3 * j + i] = Qij * isg;
         }
     }

@@ -401,15 +401,16 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     }
     if (!(tau > 0.0)) return;
 
-    // --- T_view linear part M = Rv R diag(sig); W = M^-1 = diag(1/sig) (Rv R)^T; c = -W mu_v
+    // --- T_view linear part M = Rv R diag(sig); W = M^-1 = diag(1/sig) R^T Rv^-1; c = -W mu_v
     double Q[9];
     mat3_mul(vp.Rv, R, Q);
     double M[9];
     for (int i = 0; i < 3; i++)
         for (int j = 0; j < 3; j++) M[3 * i + j] = Q[3 * i + j] * sig[j];
-    double Wm[9];
+    double Wm[9];  // Rv^-1 exactly (reading 37); R is orthonormal to FP64 rounding (normalised q)
     for (int j = 0; j < 3; j++)
-        for (int i = 0; i < 3; i++) Wm[3 * j + i] = Q[3 * i + j] * isig[j];
+        for (int i = 0; i < 3; i++)
+            Wm[3 * j + i] = (R[j] * vp.Rvi[i] + R[3 + j] * vp.Rvi[3 + i] + R[6 + j] * vp.Rvi[6 + i]) * isig[j];
     double c[3];
     mat3_vec(Wm, muv, c);
     for (int i = 0; i < 3; i++) c[i] = -c[i];

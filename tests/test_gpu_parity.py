@@ -420,3 +420,19 @@ def test_render_band_equals_full_frame(R, cfg, world):
     assert [(int(a), int(b)) for a, b in zip(cuts0[:-1], cuts0[1:])] == want_cuts
     got = np.concatenate(rows, axis=0).astype(np.float64)
     assert np.array_equal(got, full)
+
+
+@pytest.mark.parametrize("cfg,view", [("c2", 5), ("c4zoomout", 10)])
+def test_giant_list_path_bit_identical(R, cfg, view):
+    """Tiles on the giant-list path (every pixel one K6s warp from the list start) give the same
+    image bit for bit as the sub-tile K6 path (same arithmetic, same exact order)."""
+    scene, cams = S.make_config(cfg)
+    cam = cams[view]
+    R.load(scene)
+    a = _img(R, cam)
+    R.set_config(flags=pkg.AAA_FLAG_FORCE_GIANT)
+    b = _img(R, cam)
+    st = R.stats()
+    R.set_config(flags=0)
+    assert st["giant_pixels"] > 0.5 * cam.width * cam.height * 0.1 and st["unresolved_pixels"] == 0, st
+    assert np.array_equal(a, b), np.abs(a - b).max()

@@ -682,3 +682,31 @@ def test_tau_level_set_per_pixel():
                 n_straddle_in += margin > 0
                 n_straddle_out += margin < 0
     assert n_straddle_in >= 50 and n_straddle_out >= 50
+
+
+def test_camera_is_the_given_affine_map():
+    """Reading 37: the camera is the world->view map x_v = Rv x + t exactly as given. With a
+    rotation block that is deliberately not orthonormal (a row scaled by 1 + 1e-4, far beyond the
+    ~1e-7 of a float32-rounded matrix) the oracle's z* and rho^2 at a pixel still equal the paper's
+    plane pullback through T' = M_vp P V T (helpers.plane_form_rho2, forward map only): the camera
+    centre and the pixel rays use Rv^-1, not Rv^T."""
+    rng = np.random.default_rng(37)
+    V = np.eye(4)
+    ang = 0.3
+    V[:3, :3] = np.array([[np.cos(ang), 0, np.sin(ang)], [0, 1, 0], [-np.sin(ang), 0, np.cos(ang)]])
+    V[0, :3] *= 1 + 1e-4
+    V[:3, 3] = [0.4, -0.2, 2.5]
+    V = V.astype(np.float32).astype(np.float64)
+    cam = pinhole(W=48, H=48, f=60.0, V=V, near=0.01)
+    for _ in range(5):
+        mu = rng.uniform(-0.5, 0.5, 3) + np.array([-1.2, 0.2, 0.8])
+        sc = one_gaussian(mu, rng.uniform(0.05, 0.2, 3), q=rng.standard_normal(4), o=0.9, v_train=20.0)
+        M, muv, _, _ = filtered_T_view(sc, 0, cam)
+        orc = O.Oracle(sc).set_view(cam)
+        c = orc.pixel_contribs(24, 24)
+        rows = c[c[:, CI["included"]] > 0.5]
+        if not len(rows):
+            continue
+        rho2, z = plane_form_rho2(M, muv, cam, 24.5, 24.5)
+        assert rows[0, CI["z"]] == pytest.approx(z, rel=1e-10)
+        assert rows[0, CI["rho2"]] == pytest.approx(rho2, rel=1e-8, abs=1e-10)

@@ -6,9 +6,9 @@ frames/s per OOD sub-batch, c5 single-frame ms on 1 GPU and per tile band).
 Timing: CUDA events on the caller's stream around whole batches after 3 warm-up batches; per
 stage ms from the library's AAA_FLAG_TIMING events. c5 bands: the 135 tile rows are split into 8
 cost-balanced bands (aaa_tile_row_costs -> partition.band_split, as the 8-GPU path does) and
-each band is rendered alone with aaa_render_tiles (K1 on all Gaussians, K3-K6 on the band) — the
-slowest band is the per-rank compute of the 8-GPU frame (the NCCL gather is not included: one
-GPU here)."""
+each rank's band is rendered alone with aaa_render_band (K1 on all Gaussians + the row-cost model,
+K2-K6 on the band) — the slowest band is the per-rank compute of the 8-GPU frame (the NCCL gather
+is not included: one GPU here)."""
 import json
 import sys
 from pathlib import Path
@@ -39,7 +39,6 @@ def timed(fn, reps=3, warm=3):
 def main():
     import torch
     import paper_2504_12811_b200 as pkg
-    from paper_2504_12811_b200 import partition as part
     from synth import scenes as S
 
     out_path = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "gpurun_out" / "configs.jsonl"
@@ -79,15 +78,14 @@ def main():
     H, W = cam.height, cam.width
     full = torch.empty((3, H, W), dtype=torch.float32, device="cuda:0")
     ms_full = timed(lambda: R.render(cam, out_rgb=full, with_T=False))
-    costs = R.tile_row_costs()
-    bands = part.band_split(costs, 8)
-    R.set_camera(cam)
+    buf = torch.empty((3 * H * W,), dtype=torch.float32, device="cuda:0")
     band_ms = []
-    for (b0, b1) in bands:
-        rows = min(b1 * 16, H) - b0 * 16
-        buf = torch.empty((3, rows, W), dtype=torch.float32, device="cuda:0")
-        band_ms.append(timed(lambda: R.render_tiles(b0, b1, out_rgb=buf)))
-    st = R.stats()
+    bands = None
+    for rank in range(8):
+        band_ms.append(timed(lambda: R.render_band(rank, 8, out_rgb=buf)))
+        if bands is None:
+            _, _, cuts = R.render_band(rank, 8, out_rgb=buf)
+            bands = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]
     rec = {"config": "c5", "gaussians": int(scene.means.shape[0]), "width": W, "height": H,
            "frame_ms_1gpu": ms_full, "bands_8": bands, "band_ms": band_ms, "slowest_band_ms": max(band_ms),
            "band_speedup_vs_1gpu": ms_full / max(band_ms),
