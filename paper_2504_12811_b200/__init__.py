@@ -271,7 +271,7 @@ class Renderer:
     def key_tile_shift(self) -> int:
         """Bits of the depth code in a sort key (key >> this = tile id)."""
         n_tiles = ((self.width + 15) // 16) * ((self.height + 15) // 16)
-        return min(32 - max(0, (n_tiles - 1).bit_length()), 28)
+        return min(32 - n_tiles.bit_length(), 28)  # tile ids < 2^tile_bits - 1 (aaa_internal.cuh SKEY_NONE)
 
     def spilled_pixels(self) -> np.ndarray:
         """Linear indices (y * W + x) of the pixels of the last render continued by K6s (debug)."""

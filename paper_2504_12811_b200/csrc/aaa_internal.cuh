@@ -14,6 +14,7 @@ constexpr int TILE = 16;                // 16x16 pixel tiles (reading 24)
 // over KEY_LOG_RANGE octaves above near (S = 2^key_db / KEY_LOG_RANGE codes per octave); its decode
 // near_lo 2^(dcode / S) is a lower bound of z_lb, so the key stays a valid depth lower bound.
 using skey_t = uint32_t;
+constexpr skey_t SKEY_NONE = 0xFFFFFFFFu;  // K3 dense emission: culled candidate (sorts last)
 constexpr double KEY_LOG_RANGE = 24.0;
 constexpr int RASTER_REC_F4 = 7;        // raster record: 7 float4 = 112 B
 constexpr float ANGLE_EPS = 1e-4f;      // Eq. 17 epsilon (reading 17)
@@ -46,7 +47,8 @@ struct ViewParams {
     float key_near_f;      // near_lo rounded down (decode)
     double inv_fx, inv_fy; // 1/fx, 1/fy
     double key_zmul;       // (1 - ZKEY_PAD) / key_near (encode)
-    uint32_t giant_list;   // K6: tiles whose list is longer go pixel by pixel to K6s (0 = never)
+    uint32_t giant_list;   // K6: tiles whose list is longer go pixel by pixel to K6s (0 = the automatic
+                           // threshold k_tile_order computes; UINT32_MAX = never)
 };
 
 // Scene residency (L0): structure of float4 arrays, 16-byte aligned.
@@ -115,16 +117,17 @@ struct ViewBufs {
 constexpr int AAA_SP_CAP_LVL1 = AAA_SP_CAP;
 constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_SPILL = 4, CNT_SPILL_TICKET = 5,
               CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
-              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_TOTAL = 40;
+              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_GIANT_THR = 35, CNT_TOTAL = 40;
 
 // ---- launchers (each file implements its own) ----
 void launch_load_pack(const aaa_gaussians& in, const float* dmeans, const float* dscales, const float* dquats,
                       const float* dopac, const float* dsh, const float* dvt, SceneDev& sc, int64_t* d_bad,
                       cudaStream_t st);
-void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bool debug, cudaStream_t st);
+int launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bool debug, cudaStream_t st);  // launches
 size_t scan_state_words(int64_t n);
 void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, uint32_t* state, uint32_t* ticket,
                  cudaStream_t st);
+bool cull_emit_dense();  // K3 writes all C candidates (sentinel keys for culled ones)
 void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, skey_t* keys,
                       uint32_t* vals, uint32_t* state, cudaStream_t st);
 struct SortBufs {

@@ -172,13 +172,16 @@ aaa_status check_camera(aaa_ctx* ctx, const aaa_camera* c) {
     return AAA_OK;
 }
 
-// Tiles with a list longer than this are rendered pixel by pixel (one warp per pixel, K6s) instead
-// of by 8x4 sub-tile warps (K6): on giant lists (c4 zoom-out) a sub-tile warp's serial walk is the
-// kernel's critical path. AAA_GIANT_LIST overrides (0 = off).
+// Tiles with a list longer than a threshold are rendered pixel by pixel (one warp per pixel, K6s)
+// instead of by 8x4 sub-tile warps (K6): on giant lists (c4 zoom-out) a sub-tile warp's serial walk
+// is the kernel's critical path. 0 = the automatic threshold (k_tile_order); AAA_GIANT_LIST=N fixes
+// it for A/B runs (N = 0: never).
 uint32_t giant_list_threshold() {
     static const uint32_t v = [] {
         const char* e = getenv("AAA_GIANT_LIST");
-        return e ? (uint32_t)strtoul(e, nullptr, 10) : 0u;
+        if (!e) return 0u;
+        const uint32_t n = (uint32_t)strtoul(e, nullptr, 10);
+        return n ? n : UINT32_MAX;
     }();
     return v;
 }
@@ -218,7 +221,7 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     vp.sh_degree = ctx->scene.sh_degree;
     // 32-bit sort key: tile bits + log-depth code bits (see aaa_internal.cuh)
     int tb = 0;
-    while ((1u << tb) < (uint32_t)(vp.tiles_x * vp.tiles_y)) tb++;
+    while ((1u << tb) <= (uint32_t)(vp.tiles_x * vp.tiles_y)) tb++;  // tile ids < 2^tb - 1: SKEY_NONE is never a key
     vp.key_db = std::min(32 - tb, 28);
     vp.key_scale = std::ldexp(1.0, vp.key_db) / KEY_LOG_RANGE;
     float nl = (float)(c.near_z * (1.0 - 1e-5));
@@ -434,7 +437,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     size_t s2 = scan_state_words(n);
     CU(cudaMemsetAsync(sl.vb.scan_state, 0, s2 * sizeof(uint32_t), ps));
     mark(0, ps);
-    launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
+    const int k1_launches = launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
     if (band_world > 0) {
         std::vector<int64_t> cost;
         s = row_costs(ctx, sl, vp.tiles_y, ps, cost);
@@ -448,7 +451,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         if (n > 0) ctx->launches += 2;
     }
     mark(1, ps);
-    if (n > 0) ctx->launches += 2;
+    if (n > 0) ctx->launches += k1_launches + 1;  // K1 (+ K1c), K2
     launch_scan(sl.vb.counts, sl.vb.offsets, n, &sl.vb.counters[CNT_C], sl.vb.scan_state,
                 &sl.vb.counters[CNT_SCAN_TICKET], ps);
     CU(cudaGetLastError());
@@ -472,7 +475,8 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         CU(cudaGetLastError());
         return AAA_OK;
     }
-    int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_P], C, key_bits, ps);
+    // dense K3 emission: sort all C candidates (sentinels last); the first P are the kept pairs
+    int sorted = launch_sort(sl.sb, &sl.vb.counters[cull_emit_dense() ? CNT_C : CNT_P], C, key_bits, ps);
     sl.sorted = sorted;
     if (ctx->scene.perm && (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))) {
         launch_tie_fix(sl.sb.keys[sorted], sl.sb.vals[sorted], &sl.vb.counters[CNT_P], C, ctx->scene.perm, ps);
@@ -1108,6 +1112,7 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
     if (!sl.vb.counters) return fail(ctx, AAA_ERR_STATE, "no view rendered yet");
     const void* src = nullptr;
     size_t bytes = 0;
+    std::vector<unsigned char> dense_tmp;
     uint32_t h[CNT_TOTAL];
     CU(cudaMemcpy(h, sl.vb.counters, sizeof(h), cudaMemcpyDeviceToHost));
     switch (what) {
@@ -1115,8 +1120,28 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
             src = sl.vb.dbg;
             bytes = (size_t)ctx->scene.n * AAA_DBG_GAUSS_FIELDS * sizeof(double);
             break;
-        case AAA_DBG_KEYS_UNSORTED: src = sl.sb.keys[0]; bytes = (size_t)h[CNT_P] * sizeof(skey_t); break;
-        case AAA_DBG_VALS_UNSORTED: src = sl.sb.vals[0]; bytes = (size_t)h[CNT_P] * 4; break;
+        case AAA_DBG_KEYS_UNSORTED:
+        case AAA_DBG_VALS_UNSORTED:
+            if (cull_emit_dense()) {  // the kept pairs in emission order: compact the candidate array
+                std::vector<skey_t> k(h[CNT_C]);
+                std::vector<uint32_t> v(h[CNT_C]);
+                if (h[CNT_C]) {
+                    CU(cudaMemcpy(k.data(), sl.sb.keys[0], k.size() * sizeof(skey_t), cudaMemcpyDeviceToHost));
+                    CU(cudaMemcpy(v.data(), sl.sb.vals[0], v.size() * 4, cudaMemcpyDeviceToHost));
+                }
+                size_t m = 0;
+                for (size_t i = 0; i < k.size(); i++)
+                    if (k[i] != SKEY_NONE) { k[m] = k[i]; v[m] = v[i]; m++; }
+                dense_tmp.resize(m * 4);
+                if (what == AAA_DBG_KEYS_UNSORTED) memcpy(dense_tmp.data(), k.data(), m * 4);
+                else memcpy(dense_tmp.data(), v.data(), m * 4);
+                src = nullptr;
+                bytes = m * 4;
+            } else {
+                src = what == AAA_DBG_KEYS_UNSORTED ? (const void*)sl.sb.keys[0] : (const void*)sl.sb.vals[0];
+                bytes = (size_t)h[CNT_P] * 4;
+            }
+            break;
         case AAA_DBG_KEYS: src = sl.sb.keys[sl.sorted]; bytes = (size_t)h[CNT_P] * sizeof(skey_t); break;
         case AAA_DBG_VALS: src = sl.sb.vals[sl.sorted]; bytes = (size_t)h[CNT_P] * 4; break;
         case AAA_DBG_RANGES: src = sl.ranges; bytes = (size_t)sl.vp.tiles_x * sl.vp.tiles_y * sizeof(uint2); break;
@@ -1130,6 +1155,7 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
     *len = bytes;
     if (bytes > cap) return fail(ctx, AAA_ERR_INVALID_ARG, "debug buffer too small");
     if (bytes && src) CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    if (bytes && !src) memcpy(dst, dense_tmp.data(), bytes);
     // records and indices in the caller's Gaussian order (the scene is stored in Morton order)
     const std::vector<uint32_t>& pm = ctx->h_perm;
     if (bytes && !pm.empty()) {

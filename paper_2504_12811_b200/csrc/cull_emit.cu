@@ -17,6 +17,14 @@
 namespace aaa {
 
 constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS, EMIT_SOFF = 4096;
+#ifndef AAA_K3_DENSE
+#define AAA_K3_DENSE 1
+#endif
+// AAA_K3_DENSE: every candidate c writes its (key, value) at position c, culled candidates the
+// sentinel key SKEY_NONE (above every valid key: tile ids < 2^tile_bits - 1), and the kept count
+// is one atomic per block. No scan and no decoupled look-back between blocks: the onesweep sort
+// over all C candidates moves the sentinels behind the P kept pairs and keeps the kept pairs in
+// the same stable order as the compacted emission (so the sorted list is the same bit for bit).
 
 #ifndef AAA_K3_MINB
 #define AAA_K3_MINB 3  // 80 registers, 3 CTAs of 256 threads per SM (A/B on c3: 2 -> 0.70 ms, 3 -> 0.64 ms)
@@ -33,8 +41,13 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     __shared__ uint32_t s_off[EMIT_SOFF];
     // per-thread emitted pairs, [item][thread] (a register array indexed in a rolled loop would
     // live in local memory)
+#if AAA_K3_DENSE
+    __shared__ skey_t s_key[EMIT_THREADS * 9];  // [t * 9 + k]: conflict-free writes, coalesced reads
+    __shared__ uint32_t s_val[EMIT_THREADS * 9];
+#else
     __shared__ skey_t s_key[EMIT_ITEMS][EMIT_THREADS];
     __shared__ uint32_t s_val[EMIT_ITEMS][EMIT_THREADS];
+#endif
     if (threadIdx.x == 0) s_ticket = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -156,6 +169,12 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
             const CrossRec& cr = cross[r.cross_slot];
             keep = frustum_qp_min(cr.M, cr.muv, vp.fx, vp.fy, vp.cx, vp.cy, vp.near_z, x0, x1, y0, y1) < cr.tau;
         }
+#if AAA_K3_DENSE
+        const uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
+        s_key[threadIdx.x * 9 + k] = keep ? ((tile << vp.key_db) | r.zkey) : SKEY_NONE;
+        s_val[threadIdx.x * 9 + k] = keep ? ((uint32_t)g | (sub << VAL_INDEX_BITS)) : 0u;
+        nkeep += keep;
+#else
         if (keep) {
             uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
             s_key[k][threadIdx.x] = (tile << vp.key_db) | r.zkey;
@@ -163,7 +182,24 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
             keep_mask |= 1u << k;
             nkeep++;
         }
+#endif
     }
+#if AAA_K3_DENSE
+    {
+        __syncthreads();
+        const uint32_t c0 = chunk * EMIT_CHUNK;
+        for (int i = threadIdx.x; i < EMIT_CHUNK; i += EMIT_THREADS) {
+            if (c0 + i >= C) break;
+            keys[c0 + i] = s_key[(i >> 3) * 9 + (i & 7)];
+            vals[c0 + i] = s_val[(i >> 3) * 9 + (i & 7)];
+        }
+        uint32_t w = nkeep;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(&counters[CNT_P], w);
+        return;
+    }
+#else
     uint32_t btot;
     uint32_t texcl = block_exclusive_scan(nkeep, s_scan, &btot);
     if (threadIdx.x < 32) {
@@ -181,7 +217,10 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         }
     }
     if (threadIdx.x == 0 && (uint64_t)(chunk + 1) * EMIT_CHUNK >= C) counters[CNT_P] = s_excl + btot;
+#endif
 }
+
+bool cull_emit_dense() { return AAA_K3_DENSE != 0; }
 
 void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, skey_t* keys,
                       uint32_t* vals, uint32_t* state, cudaStream_t st) {

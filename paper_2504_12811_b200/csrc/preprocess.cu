@@ -348,6 +348,9 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 #define AAA_K1_MINB 3  // 168 registers: 3 CTAs of 128 threads per SM (A/B: 0.78 -> 0.69 ms on c3)
 #endif
 // DBG: the parity-test instantiation that also writes the per-Gaussian debug fields
+#ifndef AAA_K1_SPLIT
+#define AAA_K1_SPLIT 1
+#endif
 template <bool DBG>
 __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, ViewParams vp, ViewBufs vb) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -571,11 +574,15 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     rr[5] = make_float4((float)wb[1], (float)wb[2], (float)dot3(c, wref), (float)dot3(c, wa));
     rr[6] = make_float4((float)dot3(c, wb), (float)c[0], (float)c[1], (float)c[2]);  // c: backward only
 
-    // --- colour (reading 15): SH at d = (mu - o)/|mu - o| (after the record writes, so the FP64
-    // geometry is dead while the 48 SH coefficients are live: fewer registers, more resident warps)
-    float rgb[3];
-    sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
-    vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+    // --- colour (reading 15): SH at d = (mu - o)/|mu - o|. By default a separate streaming kernel
+    // (K1c, k_color) evaluates it for the visible Gaussians: K1 is latency-bound at 12 warps per SM
+    // (168 registers of FP64 geometry), and the 192 B of SH per Gaussian were its largest source
+    // of memory stalls; K1c runs at full occupancy. Same d, same arithmetic: identical colours.
+    float rgb[3] = {0.f, 0.f, 0.f};
+    if (DBG || !AAA_K1_SPLIT) {
+        sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
+        vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+    }
 
     uint32_t cnt = (ty0 <= ty1) ? (uint32_t)(tx1 - tx0 + 1) * (uint32_t)(ty1 - ty0 + 1) : 0u;
     vb.counts[g] = cnt;
@@ -592,16 +599,36 @@ __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, Vi
     }
 }
 
-void launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bool debug, cudaStream_t st) {
-    if (sc.n == 0) return;
+// K1c: SH colour of every Gaussian K1 kept (count > 0; the debug instantiation of K1 computes it
+// inline) — d in FP64 exactly as K1 computes it, then the same FP32 evaluation
+__global__ void __launch_bounds__(256) k_color(SceneDev sc, ViewParams vp, ViewBufs vb) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= sc.n || vb.counts[g] == 0) return;
+    const float4 A4 = __ldg(&sc.geomA[g]);
+    double d[3] = {(double)A4.x - vp.o[0], (double)A4.y - vp.o[1], (double)A4.z - vp.o[2]};
+    const double idn = 1.0 / sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    for (int i = 0; i < 3; i++) d[i] *= idn;
+    float rgb[3];
+    sh_color(sc.sh, sc.n, g, sc.sh_degree, make_float3((float)d[0], (float)d[1], (float)d[2]), rgb);
+    vb.color[g] = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+}
+
+int launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bool debug, cudaStream_t st) {
+    if (sc.n == 0) return 0;
     int threads = 128;
     unsigned blocks = (unsigned)((sc.n + threads - 1) / threads);
-    if (vp.flags & AAA_FLAG_NO_3D)
+    if (vp.flags & AAA_FLAG_NO_3D) {
         k_preprocess_2d<<<blocks, threads, 0, st>>>(sc, vp, vb);
-    else if (debug)
+    } else if (debug) {
         k_preprocess<true><<<blocks, threads, 0, st>>>(sc, vp, vb);
-    else
+    } else {
         k_preprocess<false><<<blocks, threads, 0, st>>>(sc, vp, vb);
+        if (AAA_K1_SPLIT) {
+            k_color<<<(unsigned)((sc.n + 255) / 256), 256, 0, st>>>(sc, vp, vb);
+            return 2;
+        }
+    }
+    return 1;
 }
 
 // Tile-band cost model: per tile row, the number of candidate (Gaussian, rect
