@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 #endif
 // DBG: the parity-test instantiation that also writes the per-Gaussian debug fields
 #ifndef AAA_K1_SPLIT
-#define AAA_K1_SPLIT 1
+#define AAA_K1_SPLIT 0  // A/B on c3: K1 0.410 ms inline vs K1 + K1c 0.455 ms split
 #endif
 template <bool DBG>
 __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, ViewParams vp, ViewBufs vb) {

@@ -42,11 +42,15 @@ def main():
     st = R.stats()
     R.set_config(flags=0)
     cnt = []
+    maxlist = []
     for c in cams[:: max(1, len(cams) // 4)]:
         R.render(c, with_T=False)
         cnt.append(R.stats())
+        rg = R.ranges()
+        maxlist.append(int((rg[:, 1].astype("int64") - rg[:, 0]).max()))
     mean = {k: sum(s[k] for s in cnt) / len(cnt) for k in
             ("pairs", "evaluations", "spilled_pixels", "giant_pixels", "deep_pixels", "unresolved_pixels")}
+    mean["max_list"] = maxlist
     env = {k: v for k, v in os.environ.items() if k.startswith("AAA_")}
     print(json.dumps({"config": cfg, "env": env, "views": len(cams), "fps": len(cams) / (best / 1e3),
                       "ms_per_view": best / len(cams),
