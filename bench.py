@@ -320,7 +320,7 @@ def workload_name(args, n, W, H):
 
 def roofline_and_stages(R, views, n, deg, st_timed, abl, pkg):
     """Per-stage algorithmic GB/s and the dominant kernel's roofline (K6: FP32 ALU)."""
-    R.set_config(flags=abl)
+    R.set_config(flags=abl)  # keeps the ablation's k
     samp = []
     for v in views[:: max(1, len(views) // 5)][:5]:
         R.render(v, with_T=False)
@@ -388,8 +388,10 @@ def run_ours(args, world, rank, local):
     del scene_t
     torch.cuda.empty_cache()
     abl = {"none": 0, "no_cull": pkg.AAA_FLAG_NO_TILE_CULL, "no_hier": pkg.AAA_FLAG_NO_HIER_SORT,
-           "no_3d": pkg.AAA_FLAG_NO_3D}[args.ablation]
-    R.set_config(flags=pkg.AAA_FLAG_TIMING | abl, window_k=int(os.environ.get("AAA_WINDOW_K", "32")))
+           "no_3d": pkg.AAA_FLAG_NO_3D, "3dgs": pkg.AAA_FLAG_NO_3D | pkg.AAA_FLAG_NO_TILE_CULL}[args.ablation]
+    # "3dgs": Table 5's MCMC / 3DGS-rasterizer row — 2D splats, no 3D culling, no 3D filter
+    R.set_config(flags=pkg.AAA_FLAG_TIMING | abl, window_k=int(os.environ.get("AAA_WINDOW_K", "32")),
+                 k=0.0 if args.ablation == "3dgs" else 0.3)
     stream = torch.cuda.current_stream(dev)
     if args.config == "c5":
         res = bands_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n)
@@ -580,8 +582,9 @@ def main():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ablation", default="none", choices=["none", "no_cull", "no_hier", "no_3d"],
-                    help="Table 5 switches (P:521-524): no 3D tile culling / no per-pixel re-sort / 2D splats")
+    ap.add_argument("--ablation", default="none", choices=["none", "no_cull", "no_hier", "no_3d", "3dgs"],
+                    help="Table 5 switches (P:521-525): no 3D tile culling / no per-pixel re-sort / 2D splats / "
+                         "the 3DGS-style baseline (2D splats, no 3D culling, k = 0)")
     args = ap.parse_args()
     rc = self_launch(args)
     if rc is not None:

@@ -351,10 +351,41 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 #ifndef AAA_K1_SPLIT
 #define AAA_K1_SPLIT 0  // A/B on c3: K1 0.410 ms inline vs K1 + K1c 0.455 ms split
 #endif
+#ifndef AAA_K1_ITEMS
+#define AAA_K1_ITEMS 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+template <bool DBG>
+__device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, int64_t g);
+
+// K1 is latency-bound at 12 warps per SM (FP64 registers). AAA_K1_ITEMS > 1: each thread walks
+// AAA_K1_ITEMS Gaussians grid-strided and prefetches the next one's geometry (L1) and SH (L2)
+// before working on the current one, so its loads are in flight during the FP64 work.
 template <bool DBG>
 __global__ void __launch_bounds__(128, AAA_K1_MINB) k_preprocess(SceneDev sc, ViewParams vp, ViewBufs vb) {
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= sc.n) return;
+    if (AAA_K1_ITEMS == 1) {
+        const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (g < sc.n) k1_one<DBG>(sc, vp, vb, g);
+        return;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < sc.n; g += stride) {
+        if (AAA_K1_ITEMS > 1 && g + stride < sc.n) {
+            const int64_t gn = g + stride;
+            prefetch_l1(&sc.geomA[gn]);
+            prefetch_l1(&sc.geomB[gn]);
+            prefetch_l1(&sc.geomC[gn]);
+            const int chunks = (3 * (sc.sh_degree + 1) * (sc.sh_degree + 1) + 3) / 4;
+            for (int c = 0; c < chunks; c++) prefetch_l2(&sc.sh[(int64_t)c * sc.n + gn]);
+        }
+        k1_one<DBG>(sc, vp, vb, g);
+    }
+}
+
+template <bool DBG>
+__device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, int64_t g) {
     const double INF = CUDART_INF;
     float4 A4 = __ldg(&sc.geomA[g]), B4 = __ldg(&sc.geomB[g]), C4 = __ldg(&sc.geomC[g]);
     double* dbg = DBG ? vb.dbg + g * AAA_DBG_GAUSS_FIELDS : nullptr;
@@ -622,7 +653,8 @@ int launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bo
     } else if (debug) {
         k_preprocess<true><<<blocks, threads, 0, st>>>(sc, vp, vb);
     } else {
-        k_preprocess<false><<<blocks, threads, 0, st>>>(sc, vp, vb);
+        const unsigned b1 = (unsigned)((sc.n + threads * AAA_K1_ITEMS - 1) / (threads * AAA_K1_ITEMS));
+        k_preprocess<false><<<b1, threads, 0, st>>>(sc, vp, vb);
         if (AAA_K1_SPLIT) {
             k_color<<<(unsigned)((sc.n + 255) / 256), 256, 0, st>>>(sc, vp, vb);
             return 2;

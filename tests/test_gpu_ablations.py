@@ -106,3 +106,26 @@ def test_no_3d_matches_oracle_2d_splat(R, cfg, view):
     rep2 = compare(orc, img2.reshape(-1, 4), xx.ravel(), yy.ravel())
     assert rep2["ok"], rep2
     assert (np.abs(img - img2).max(axis=2) > 0).mean() < 1e-3
+
+
+@pytest.mark.parametrize("cfg,view", [("c1", 0), ("c2", 12)])
+def test_3dgs_style_baseline_matches_oracle(R, cfg, view):
+    """Table 5's "MCMC (3DGS rasterizer)" row as this renderer's
+    3DGS-style baseline: 2D EWA splats (NO_3D), no 3D tile culling (NO_TILE_CULL), no adaptive
+    filter (k = 0), the global mean-depth order — against the oracle in eval_mode 1 with k = 0."""
+    scene, cams = S.make_config(cfg)
+    cam = cams[view]
+    R.load(scene)
+    try:
+        R.set_config(flags=pkg.AAA_FLAG_NO_3D | pkg.AAA_FLAG_NO_TILE_CULL, k=0.0)
+        img = _img(R, cam)
+        st = R.stats()
+        R.set_camera(cam)
+        kp = _key_params(R, cam)
+    finally:
+        R.set_config(flags=0, k=0.3)
+    assert st["pairs"] == st["candidates"] > 0
+    orc = O.Oracle(scene).set_view(cam, eval_mode=1, k=0.0, **kp)
+    yy, xx = np.mgrid[0:cam.height, 0:cam.width]
+    rep = compare(orc, img.reshape(-1, 4), xx.ravel(), yy.ravel())
+    assert rep["ok"], rep

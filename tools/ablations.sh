@@ -1,8 +1,8 @@
 #!/bin/bash
 # Table 5 analogue on c3: the same kernels with each ablation switch; one JSON line each
-R=${1:-r01}
-for a in none no_cull no_hier no_3d; do
-  timeout 900 python bench.py --steps 3 --warmup 3 --views-per-rank 10 --no-cpu-baseline --no-e2e --ablation $a \
+R=${1:-r02}
+for a in none no_cull no_hier no_3d 3dgs; do
+  timeout 900 python bench.py --steps 3 --warmup 3 --scaling weak --views-per-rank 10 --no-cpu-baseline --no-e2e --ablation $a \
     >> gpurun_out/ablations_${R}.jsonl 2> gpurun_out/ablation_${a}.err || tail -3 gpurun_out/ablation_${a}.err
 done
 python - <<PY
