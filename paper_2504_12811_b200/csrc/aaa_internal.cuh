@@ -15,7 +15,14 @@ constexpr int TILE = 16;                // 16x16 pixel tiles (reading 24)
 // near_lo 2^(dcode / S) is a lower bound of z_lb, so the key stays a valid depth lower bound.
 using skey_t = uint32_t;
 constexpr skey_t SKEY_NONE = 0xFFFFFFFFu;  // K3 dense emission: culled candidate (sorts last)
-constexpr double KEY_LOG_RANGE = 24.0;
+#ifndef AAA_KEY_BITS
+#define AAA_KEY_BITS 32  // sort key width: 8-bit radix passes = AAA_KEY_BITS / 8
+#endif
+#ifndef AAA_KEY_LOG_RANGE
+#define AAA_KEY_LOG_RANGE 24.0
+#endif
+constexpr int KEY_BITS = AAA_KEY_BITS;
+constexpr double KEY_LOG_RANGE = AAA_KEY_LOG_RANGE;
 constexpr int RASTER_REC_F4 = 7;        // raster record: 7 float4 = 112 B
 constexpr float ANGLE_EPS = 1e-4f;      // Eq. 17 epsilon (reading 17)
 constexpr double ZKEY_PAD = 1e-5;       // relative downward pad of the depth key (reading 23)

@@ -222,7 +222,7 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     // 32-bit sort key: tile bits + log-depth code bits (see aaa_internal.cuh)
     int tb = 0;
     while ((1u << tb) <= (uint32_t)(vp.tiles_x * vp.tiles_y)) tb++;  // tile ids < 2^tb - 1: SKEY_NONE is never a key
-    vp.key_db = std::min(32 - tb, 28);
+    vp.key_db = std::min(KEY_BITS - tb, 28);
     vp.key_scale = std::ldexp(1.0, vp.key_db) / KEY_LOG_RANGE;
     float nl = (float)(c.near_z * (1.0 - 1e-5));
     if ((double)nl > c.near_z * (1.0 - 1e-5)) nl = std::nextafter(nl, 0.f);
@@ -459,7 +459,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     CU(cudaMemcpyAsync(ctx->h_counters, sl.vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ps));
     CU(cudaStreamSynchronize(ps));
     const uint32_t C = ctx->h_counters[CNT_C];
-    const int key_bits = 32;
+    const int key_bits = KEY_BITS;
     s = ensure_pairs(ctx, sl, C);
     if (s) return s;
     mark(3, ps);

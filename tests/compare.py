@@ -26,9 +26,11 @@ def _variants(c, cfg):
     flippable = (flags & (O.F_CUTOFF | O.F_NEAR | O.F_GAUSS)) != 0
     seq = [i for i in range(n) if inc0[i] or flippable[i]]
     z = c[:, CI["z"]]
-    # FP32 depths carry <= ~3e-7 relative error, so only neighbours closer than TIGHT can swap;
-    # the oracle's tie flag (band_tie = 4e-6) marks a superset of those pixels
-    TIGHT = min(cfg["band_tie"], 6e-7)  # 2 x the measured max FP32 z error (2.5e-7)
+    # Neighbours whose float64 depths are closer than the tie band (delta_t =
+    # 4e-6 relative) may swap: K6 evaluates z* in FP32 from an affine form re-centred at p_ref, whose
+    # error is ~2^-24 times its condition number (|c.w_ref| + |dx c.a| + |dy c.b|) / |c.w| — up to
+    # 4e-7 per depth measured on the c5 4K frame, so a 6.2e-7 gap flipped there.
+    TIGHT = cfg["band_tie"]
     clusters, cur = [], [seq[0]] if seq else []
     # global-order mode (Table 5 "w/o hier. sort"): the order is the key order, exact on both sides
     pairs = zip(seq[:-1], seq[1:]) if cfg.get("order_mode", 0) == 0 else []
