@@ -180,9 +180,11 @@ aaa_status aaa_load_gaussians(aaa_ctx* ctx, const aaa_gaussians* g, int64_t* fir
 aaa_status aaa_set_camera(aaa_ctx* ctx, const aaa_camera* cam);
 
 /* Render the current camera. rgb: 3 x H x W float32 (CHW), T: H x W final transmittance
- * (nullable). Pointers may be device memory (rendered in place, asynchronous on the
- * context's stream) or host memory (copied back; the call returns after the copy).
- * The call synchronises once internally to size the pair buffers. */
+ * (nullable). Pointers may be device memory (rendered in place on the context's stream) or host
+ * memory (copied back; the call returns after the copy). The views themselves need no host round
+ * trip (K3 and the sort read the candidate count on the device); the call synchronises once at its
+ * end to check that no view outgrew the context's pair buffers, and renders any that did again
+ * with larger buffers (the first call of a context also reads the count back once per slot). */
 aaa_status aaa_render(aaa_ctx* ctx, float* rgb, float* T);
 
 /* Render n_views cameras (all with the same width/height) into rgb n x 3 x H x W and

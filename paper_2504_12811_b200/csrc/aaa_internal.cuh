@@ -124,7 +124,7 @@ struct ViewBufs {
 constexpr int AAA_SP_CAP_LVL1 = AAA_SP_CAP;
 constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_SPILL = 4, CNT_SPILL_TICKET = 5,
               CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
-              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_GIANT_THR = 35, CNT_TOTAL = 40;
+              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_GIANT_THR = 35, CNT_CCLAMP = 36, CNT_TOTAL = 40;
 
 // ---- launchers (each file implements its own) ----
 void launch_load_pack(const aaa_gaussians& in, const float* dmeans, const float* dscales, const float* dquats,
@@ -134,9 +134,9 @@ int launch_preprocess(const SceneDev& sc, const ViewParams& vp, ViewBufs& vb, bo
 size_t scan_state_words(int64_t n);
 void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total, uint32_t* state, uint32_t* ticket,
                  cudaStream_t st);
-bool cull_emit_dense();  // K3 writes all C candidates (sentinel keys for culled ones)
-void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, skey_t* keys,
-                      uint32_t* vals, uint32_t* state, cudaStream_t st);
+// K3 over the first min(C, cap) candidates (C read on the device); raises *ovf when C > cap
+void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t cap, skey_t* keys,
+                      uint32_t* vals, uint32_t* ovf, cudaStream_t st);
 struct SortBufs {
     skey_t* keys[2];
     uint32_t* vals[2];

@@ -1,8 +1,10 @@
 // api.cu — the C ABI (include/aaa.h): context, scene residency, per-view pipeline driver.
 //
 // Pipeline per view:
-//   compute stream: K1 preprocess -> K2 scan -> [one 16-byte D2H of the counters, the only host
-//                   sync] -> K3 cull+emit -> K4 onesweep sort -> K5 ranges -> K6 raster -> K6s
+//   compute stream: K1 preprocess -> K2 scan -> K3 cull+emit (candidate count read on the device,
+//                   grid over the pair capacity) -> K4 onesweep sort -> K5 ranges -> K6 raster -> K6s
+//   (one host synchronisation per call, at its end: views whose candidates outgrew the pair
+//   buffers are rendered again with larger ones)
 //   copy stream:    (host outputs) D2H of the image, overlapping the next view's kernels
 // Every per-view buffer lives in one of two slots used alternately; the events prep_done /
 // raster_done of a slot order the two streams. (Running view v+1's K1-K5 concurrently with view
@@ -97,6 +99,11 @@ struct aaa_ctx {
     float* bwd_acc = nullptr;
     size_t bwd_acc_cap = 0;
     // tile-band cost model (aaa_render_band / aaa_tile_row_costs): device row difference array
+    // per-call overflow words of the views (K3: candidate count above the pair capacity), host copy
+    uint32_t* d_ovf = nullptr;
+    size_t ovf_cap = 0;
+    std::vector<uint32_t> h_ovf;
+    uint32_t c_hint = 0;  // pair capacity the last overflow asked for
     unsigned long long* d_rowdiff = nullptr;
     unsigned long long* h_rowdiff = nullptr;  // pinned
     int rowdiff_cap = 0;
@@ -406,7 +413,8 @@ void split_bands(const std::vector<int64_t>& cost, int world, int32_t* cuts) {
 // of the cost-balanced split (cuts written to band_cuts).
 aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_end, float* rgb, float* T,
                     float* host_rgb, float* host_T, bool debug_k1, int stop_after, int band_rank = -1,
-                    int band_world = 0, int32_t* band_cuts = nullptr) {
+                    int band_world = 0, int32_t* band_cuts = nullptr, uint32_t* ovf = nullptr,
+                    bool sync_size = false) {
     Slot& sl = ctx->slot[ctx->cur];
     cudaStream_t ps = ctx->pstream, rs = ctx->rstream;
     const int64_t n = ctx->scene.n;
@@ -456,36 +464,40 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
                 &sl.vb.counters[CNT_SCAN_TICKET], ps);
     CU(cudaGetLastError());
     mark(2, ps);
-    CU(cudaMemcpyAsync(ctx->h_counters, sl.vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ps));
-    CU(cudaStreamSynchronize(ps));
-    const uint32_t C = ctx->h_counters[CNT_C];
+    // The pair buffers keep the capacity earlier views needed: K3 and the sort read the candidate
+    // count C on the device and size nothing from it on the host, so a view costs no host round
+    // trip. The first view of a slot, debug views and re-renders (sync_size) read C back once to
+    // size the buffers; a view whose C exceeds the capacity raises *ovf and the call re-renders it
+    // after growing them (render_common).
+    if (sync_size || sl.pair_cap == 0 || stop_after == 1 || ctx->c_hint > sl.pair_cap) {
+        CU(cudaMemcpyAsync(ctx->h_counters, sl.vb.counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ps));
+        CU(cudaStreamSynchronize(ps));
+        s = ensure_pairs(ctx, sl, std::max(ctx->h_counters[CNT_C], ctx->c_hint));
+        if (s) return s;
+    }
+    const uint32_t cap = sl.pair_cap;
     const int key_bits = KEY_BITS;
-    s = ensure_pairs(ctx, sl, C);
-    if (s) return s;
     mark(3, ps);
-    size_t emit_words = (size_t)C / 2048 + 2;
-    CU(cudaMemsetAsync(sl.vb.scan_state, 0, emit_words * sizeof(uint32_t), ps));
-    launch_cull_emit(vp, sl.vb, n, C, sl.sb.keys[0], sl.sb.vals[0], sl.vb.scan_state, ps);
+    launch_cull_emit(vp, sl.vb, n, cap, sl.sb.keys[0], sl.sb.vals[0], ovf, ps);
     mark(4, ps);
-    if (C > 0) ctx->launches += 1;
+    ctx->launches += 1;
     sl.vp = vp;
-    sl.C = C;
     if (stop_after == 1) {
         sl.sorted = 0;
         CU(cudaGetLastError());
         return AAA_OK;
     }
-    // dense K3 emission: sort all C candidates (sentinels last); the first P are the kept pairs
-    int sorted = launch_sort(sl.sb, &sl.vb.counters[cull_emit_dense() ? CNT_C : CNT_P], C, key_bits, ps);
+    // sort all min(C, cap) candidates (dense K3 emission: sentinels last, the first P are kept pairs)
+    int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_CCLAMP], cap, key_bits, ps);
     sl.sorted = sorted;
     if (ctx->scene.perm && (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))) {
-        launch_tie_fix(sl.sb.keys[sorted], sl.sb.vals[sorted], &sl.vb.counters[CNT_P], C, ctx->scene.perm, ps);
+        launch_tie_fix(sl.sb.keys[sorted], sl.sb.vals[sorted], &sl.vb.counters[CNT_P], cap, ctx->scene.perm, ps);
         ctx->launches += 1;
     }
     mark(5, ps);
-    launch_ranges(sl.sb.keys[sorted], &sl.vb.counters[CNT_P], C, sl.ranges, vp.tiles_x * vp.tiles_y, vp.key_db, ps);
+    launch_ranges(sl.sb.keys[sorted], &sl.vb.counters[CNT_P], cap, sl.ranges, vp.tiles_x * vp.tiles_y, vp.key_db, ps);
     mark(6, ps);
-    if (C > 0) ctx->launches += 3 + sort_passes(key_bits);
+    ctx->launches += 3 + sort_passes(key_bits);
     const int out_h = std::min(row_end * TILE, cam.height) - row_begin * TILE;
     const size_t plane = (size_t)out_h * cam.width;
     RasterArgs ra{};
@@ -619,13 +631,44 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
     ctx->saved = false;
     aaa_status s = enter(ctx);
     if (s) return s;
+    if ((size_t)n_views > ctx->ovf_cap) {
+        cudaFree(ctx->d_ovf);
+        ctx->d_ovf = nullptr;
+        ctx->ovf_cap = 0;
+        CU(cudaMalloc(&ctx->d_ovf, (size_t)n_views * sizeof(uint32_t)));
+        ctx->ovf_cap = (size_t)n_views;
+    }
+    CU(cudaMemsetAsync(ctx->d_ovf, 0, (size_t)n_views * sizeof(uint32_t), ctx->pstream));
+    auto view_ptrs = [&](int v, float*& r, float*& t, float*& hr, float*& ht) {
+        r = dev_rgb ? rgb + 3 * plane * v : nullptr;
+        t = T && dev_T ? T + plane * v : nullptr;
+        hr = dev_rgb ? nullptr : rgb + 3 * plane * v;
+        ht = T && !dev_T ? T + plane * v : nullptr;
+    };
     for (int v = 0; v < n_views && !s; v++) {
         ctx->cur ^= 1;
-        float* r = dev_rgb ? rgb + 3 * plane * v : nullptr;
-        float* t = T && dev_T ? T + plane * v : nullptr;
-        float* hr = dev_rgb ? nullptr : rgb + 3 * plane * v;
-        float* ht = T && !dev_T ? T + plane * v : nullptr;
-        s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0, band_rank, band_world, band_cuts);
+        float *r, *t, *hr, *ht;
+        view_ptrs(v, r, t, hr, ht);
+        s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0, band_rank, band_world, band_cuts,
+                     ctx->d_ovf + v);
+    }
+    if (!s) {
+        // the call's one host synchronisation: did any view need more pair capacity than its slot
+        // had (K3 then covered only part of its candidates)? Those views are rendered again with
+        // buffers sized from their own count.
+        ctx->h_ovf.resize((size_t)n_views);
+        CU(cudaMemcpyAsync(ctx->h_ovf.data(), ctx->d_ovf, (size_t)n_views * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           ctx->pstream));
+        CU(cudaStreamSynchronize(ctx->pstream));
+        for (int v = 0; v < n_views && !s; v++) {
+            if (!ctx->h_ovf[v]) continue;
+            ctx->c_hint = std::max(ctx->c_hint, ctx->h_ovf[v]);
+            ctx->cur ^= 1;
+            float *r, *t, *hr, *ht;
+            view_ptrs(v, r, t, hr, ht);
+            s = run_view(ctx, cams[v], row_begin, row_end, r, t, hr, ht, false, 0, band_rank, band_world, band_cuts,
+                         nullptr, true);
+        }
     }
     if (save && !s) {
         // a pixel that blended more than rec_cap contributions: grow the record and render again
@@ -639,7 +682,7 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
         if (mx > ctx->rec_cap) {
             while (ctx->rec_cap < mx) ctx->rec_cap *= 2;
             s = run_view(ctx, cams[0], row_begin, row_end, dev_rgb ? rgb : nullptr, T && dev_T ? T : nullptr,
-                         dev_rgb ? nullptr : rgb, T && !dev_T ? T : nullptr, false, 0);
+                         dev_rgb ? nullptr : rgb, T && !dev_T ? T : nullptr, false, 0, -1, 0, nullptr, nullptr, true);
         }
     }
     aaa_status s2 = leave(ctx);
@@ -710,6 +753,7 @@ void aaa_destroy(aaa_ctx* ctx) {
     cudaFree(ctx->rec); cudaFree(ctx->rec_n); cudaFree(ctx->bwd_acc); cudaFree(ctx->bwd_overflow);
     cudaFree(ctx->d_rowdiff);
     if (ctx->h_rowdiff) cudaFreeHost(ctx->h_rowdiff);
+    cudaFree(ctx->d_ovf);
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev_pool)
         for (auto x : e) cudaEventDestroy(x);
@@ -1122,24 +1166,22 @@ aaa_status aaa_debug_copy(aaa_ctx* ctx, int32_t what, void* dst, size_t cap, siz
             break;
         case AAA_DBG_KEYS_UNSORTED:
         case AAA_DBG_VALS_UNSORTED:
-            if (cull_emit_dense()) {  // the kept pairs in emission order: compact the candidate array
-                std::vector<skey_t> k(h[CNT_C]);
-                std::vector<uint32_t> v(h[CNT_C]);
-                if (h[CNT_C]) {
-                    CU(cudaMemcpy(k.data(), sl.sb.keys[0], k.size() * sizeof(skey_t), cudaMemcpyDeviceToHost));
-                    CU(cudaMemcpy(v.data(), sl.sb.vals[0], v.size() * 4, cudaMemcpyDeviceToHost));
+            {  // the kept pairs in emission order: compact the candidate array (dense K3 emission)
+                const size_t cn = std::min<size_t>(h[CNT_C], sl.pair_cap);
+                std::vector<skey_t> k(cn);
+                std::vector<uint32_t> v(cn);
+                if (cn) {
+                    CU(cudaMemcpy(k.data(), sl.sb.keys[0], cn * sizeof(skey_t), cudaMemcpyDeviceToHost));
+                    CU(cudaMemcpy(v.data(), sl.sb.vals[0], cn * 4, cudaMemcpyDeviceToHost));
                 }
                 size_t m = 0;
-                for (size_t i = 0; i < k.size(); i++)
+                for (size_t i = 0; i < cn; i++)
                     if (k[i] != SKEY_NONE) { k[m] = k[i]; v[m] = v[i]; m++; }
                 dense_tmp.resize(m * 4);
                 if (what == AAA_DBG_KEYS_UNSORTED) memcpy(dense_tmp.data(), k.data(), m * 4);
                 else memcpy(dense_tmp.data(), v.data(), m * 4);
                 src = nullptr;
                 bytes = m * 4;
-            } else {
-                src = what == AAA_DBG_KEYS_UNSORTED ? (const void*)sl.sb.keys[0] : (const void*)sl.sb.vals[0];
-                bytes = (size_t)h[CNT_P] * 4;
             }
             break;
         case AAA_DBG_KEYS: src = sl.sb.keys[sl.sorted]; bytes = (size_t)h[CNT_P] * sizeof(skey_t); break;

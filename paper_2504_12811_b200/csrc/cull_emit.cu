@@ -12,19 +12,19 @@
 // of keep flags plus a decoupled look-back over candidate chunks taken in ticket order.
 #include "aaa_internal.cuh"
 #include "geom.cuh"
-#include "lookback.cuh"
 
 namespace aaa {
 
 constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS, EMIT_SOFF = 4096;
-#ifndef AAA_K3_DENSE
-#define AAA_K3_DENSE 1
-#endif
-// AAA_K3_DENSE: every candidate c writes its (key, value) at position c, culled candidates the
+// Dense emission: every candidate c writes its (key, value) at position c, culled candidates the
 // sentinel key SKEY_NONE (above every valid key: tile ids < 2^tile_bits - 1), and the kept count
 // is one atomic per block. No scan and no decoupled look-back between blocks: the onesweep sort
 // over all C candidates moves the sentinels behind the P kept pairs and keeps the kept pairs in
-// the same stable order as the compacted emission (so the sorted list is the same bit for bit).
+// the same stable order as a compacted emission would (so the sorted list is the same bit for bit;
+// A/B on c3: K3 0.425 -> 0.341 ms, sort 0.210 -> 0.242 ms against the round-1 compacting K3).
+// The candidate count C is read on the device (no host round trip): the grid covers the pair
+// buffers' capacity `cap`, chunks at or beyond C exit, and a view with C > cap only processes the
+// first cap candidates and raises *ovf (the host re-renders it with larger buffers).
 
 #ifndef AAA_K3_MINB
 #define AAA_K3_MINB 3  // 80 registers, 3 CTAs of 256 threads per SM (A/B on c3: 2 -> 0.70 ms, 3 -> 0.64 ms)
@@ -32,24 +32,28 @@ constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EM
 __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewParams vp, const CullRec* __restrict__ cull,
                                                             const CrossRec* __restrict__ cross,
                                                             const uint32_t* __restrict__ offsets, int64_t n,
-                                                            uint32_t C, skey_t* __restrict__ keys,
+                                                            uint32_t cap, skey_t* __restrict__ keys,
                                                             uint32_t* __restrict__ vals, uint32_t* counters,
-                                                            uint32_t* state) {
-    __shared__ uint32_t s_scan[32];
-    __shared__ uint32_t s_ticket, s_excl;
+                                                            uint32_t* ovf) {
+    __shared__ uint32_t s_ticket, s_C;
     __shared__ int64_t s_g0, s_g1;
     __shared__ uint32_t s_off[EMIT_SOFF];
     // per-thread emitted pairs, [item][thread] (a register array indexed in a rolled loop would
     // live in local memory)
-#if AAA_K3_DENSE
     __shared__ skey_t s_key[EMIT_THREADS * 9];  // [t * 9 + k]: conflict-free writes, coalesced reads
     __shared__ uint32_t s_val[EMIT_THREADS * 9];
-#else
-    __shared__ skey_t s_key[EMIT_ITEMS][EMIT_THREADS];
-    __shared__ uint32_t s_val[EMIT_ITEMS][EMIT_THREADS];
-#endif
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
+    if (threadIdx.x == 0) {
+        s_ticket = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
+        const uint32_t Cd = counters[CNT_C];
+        s_C = min(Cd, cap);
+        if (s_ticket == 0) {
+            counters[CNT_CCLAMP] = s_C;  // the sort's element count
+            if (Cd > cap && ovf) *ovf = Cd;  // the capacity this view needs
+        }
+    }
     __syncthreads();
+    const uint32_t C = s_C;
+    if ((uint64_t)s_ticket * EMIT_CHUNK >= C) return;
     if (threadIdx.x < 32) {
         // the chunk's candidates [c0, c1] belong to Gaussians [g0, g1] (largest g with offset <= c):
         // two 17-ary searches side by side (half-warp each), one parallel load per step
@@ -104,7 +108,7 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     } r;
     int64_t g_loaded = -1;
     QuadF qf{};
-    uint32_t keep_mask = 0, nkeep = 0;
+    uint32_t nkeep = 0;
     const bool no_cull = (vp.flags & AAA_FLAG_NO_TILE_CULL) != 0;
     const bool f64_only = (vp.flags & AAA_FLAG_CULL_FP64) != 0;  // guard-band test switch
 #pragma unroll 1
@@ -169,22 +173,11 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
             const CrossRec& cr = cross[r.cross_slot];
             keep = frustum_qp_min(cr.M, cr.muv, vp.fx, vp.fy, vp.cx, vp.cy, vp.near_z, x0, x1, y0, y1) < cr.tau;
         }
-#if AAA_K3_DENSE
         const uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
         s_key[threadIdx.x * 9 + k] = keep ? ((tile << vp.key_db) | r.zkey) : SKEY_NONE;
         s_val[threadIdx.x * 9 + k] = keep ? ((uint32_t)g | (sub << VAL_INDEX_BITS)) : 0u;
         nkeep += keep;
-#else
-        if (keep) {
-            uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
-            s_key[k][threadIdx.x] = (tile << vp.key_db) | r.zkey;
-            s_val[k][threadIdx.x] = (uint32_t)g | (sub << VAL_INDEX_BITS);
-            keep_mask |= 1u << k;
-            nkeep++;
-        }
-#endif
     }
-#if AAA_K3_DENSE
     {
         __syncthreads();
         const uint32_t c0 = chunk * EMIT_CHUNK;
@@ -199,35 +192,14 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         if ((threadIdx.x & 31) == 0 && w) atomicAdd(&counters[CNT_P], w);
         return;
     }
-#else
-    uint32_t btot;
-    uint32_t texcl = block_exclusive_scan(nkeep, s_scan, &btot);
-    if (threadIdx.x < 32) {
-        uint32_t e = lookback_warp(state, chunk, btot);
-        if (threadIdx.x == 0) s_excl = e;
-    }
-    __syncthreads();
-    uint32_t pos = s_excl + texcl;
-#pragma unroll
-    for (int k = 0; k < EMIT_ITEMS; k++) {
-        if (keep_mask & (1u << k)) {
-            keys[pos] = s_key[k][threadIdx.x];
-            vals[pos] = s_val[k][threadIdx.x];
-            pos++;
-        }
-    }
-    if (threadIdx.x == 0 && (uint64_t)(chunk + 1) * EMIT_CHUNK >= C) counters[CNT_P] = s_excl + btot;
-#endif
 }
 
-bool cull_emit_dense() { return AAA_K3_DENSE != 0; }
-
-void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t C, skey_t* keys,
-                      uint32_t* vals, uint32_t* state, cudaStream_t st) {
-    if (C == 0) return;
-    unsigned blocks = (C + EMIT_CHUNK - 1) / EMIT_CHUNK;
-    k_cull_emit<<<blocks, EMIT_THREADS, 0, st>>>(vp, vb.cull, vb.cross, vb.offsets, n, C, keys, vals, vb.counters,
-                                                 state);
+void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t cap, skey_t* keys,
+                      uint32_t* vals, uint32_t* ovf, cudaStream_t st) {
+    if (cap == 0) return;
+    unsigned blocks = (cap + EMIT_CHUNK - 1) / EMIT_CHUNK;
+    k_cull_emit<<<blocks, EMIT_THREADS, 0, st>>>(vp, vb.cull, vb.cross, vb.offsets, n, cap, keys, vals, vb.counters,
+                                                 ovf);
 }
 
 }  // namespace aaa

@@ -68,10 +68,11 @@ def _sampled_compare(R, scene, cam, n_tiles=24, per_tile=48, seed=0, loaded=Fals
 
 
 # ------------------------------------------------------------------ K1 records
-@pytest.mark.parametrize("cfg", ["c1", "c2"])
-def test_k1_records_match_oracle(R, cfg):
+@pytest.mark.parametrize("cfg,view", [("c1", 0), ("c2", 0), ("c3", 0), ("c4wide", 3), ("c4zoomout", 10),
+                                      ("c4inside", 48), ("c4inside", 49), ("c5", 0)])
+def test_k1_records_match_oracle(R, cfg, view):
     scene, cams = S.make_config(cfg)
-    cam = cams[0]
+    cam = cams[view]
     R.load(scene)
     R.set_camera(cam)
     G = R.gaussian_records()
@@ -96,6 +97,8 @@ def test_k1_records_match_oracle(R, cfg):
     # whole-view cull: GPU visible <=> oracle min rho^2 over the screen frustum < tau
     valid = live & (Go[:, FI["valid"]] > 0) & ~margin
     idx = np.nonzero(valid)[0]
+    if len(idx) > 300000:  # full-size configs: a seeded sample of the QPs
+        idx = np.sort(np.random.default_rng(view).choice(idx, 300000, replace=False))
     rect = np.tile([0.5, cam.width - 0.5, 0.5, cam.height - 0.5], (len(idx), 1))
     mn = orc.frustum_min_rho2(idx, rect)
     band = np.abs(mn - tau_o[idx]) <= 1e-5 * np.maximum(1, tau_o[idx])
