@@ -439,3 +439,25 @@ def test_giant_list_path_bit_identical(R, cfg, view):
     R.set_config(flags=0)
     assert st["giant_pixels"] > 0.5 * cam.width * cam.height * 0.1 and st["unresolved_pixels"] == 0, st
     assert np.array_equal(a, b), np.abs(a - b).max()
+
+
+def test_batch_pair_capacity_overflow_rerenders(R):
+    """A batch whose later views need more (Gaussian, tile) candidates than the pair buffers the
+    first views sized (no per-view host round trip, DESIGN 8): those views are rendered again with
+    grown buffers at the end of the call, so every image equals its own single-view render."""
+    scene, cams = S.make_config("c2")
+    base = cams[4]
+    sel = [base.scaled(fx=base.fx * 0.25, fy=base.fy * 0.25), base.scaled(fx=base.fx * 0.3, fy=base.fy * 0.3),
+           base.scaled(fx=base.fx * 1.6, fy=base.fy * 1.6), base.scaled(fx=base.fx * 2.0, fy=base.fy * 2.0)]
+    fresh = pkg.Renderer(0)
+    fresh.load(scene)
+    rgb, _ = fresh.render_batch(sel)
+    torch.cuda.synchronize()
+    cand = []
+    for i, c in enumerate(sel):
+        R.load(scene)
+        single = _img(R, c)
+        cand.append(R.stats()["candidates"])
+        assert np.array_equal(rgb[i].cpu().numpy(), single[..., :3].transpose(2, 0, 1).astype(np.float32)), i
+    assert cand[3] > 1.5 * 1.25 * cand[1], cand  # view 3 outgrew the capacity slot 1 sized
+    fresh.close()
