@@ -16,6 +16,9 @@
 namespace aaa {
 
 constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS, EMIT_SOFF = 4096;
+#ifndef AAA_K3_PERSIST
+#define AAA_K3_PERSIST 1
+#endif
 // Dense emission: every candidate c writes its (key, value) at position c, culled candidates the
 // sentinel key SKEY_NONE (above every valid key: tile ids < 2^tile_bits - 1), and the kept count
 // is one atomic per block. No scan and no decoupled look-back between blocks: the onesweep sort
@@ -42,6 +45,11 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     // live in local memory)
     __shared__ skey_t s_key[EMIT_THREADS * 9];  // [t * 9 + k]: conflict-free writes, coalesced reads
     __shared__ uint32_t s_val[EMIT_THREADS * 9];
+#if AAA_K3_PERSIST
+    // persistent CTAs (a grid of resident CTAs, independent of C): each takes chunk tickets
+    // until the chunks run out
+    for (;;) {
+#endif
     if (threadIdx.x == 0) {
         s_ticket = atomicAdd(&counters[CNT_EMIT_TICKET], 1u);
         const uint32_t Cd = counters[CNT_C];
@@ -190,14 +198,18 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
         if ((threadIdx.x & 31) == 0 && w) atomicAdd(&counters[CNT_P], w);
-        return;
     }
+#if AAA_K3_PERSIST
+    __syncthreads();  // the shared staging is reused by the next chunk
+    }
+#endif
 }
 
 void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t cap, skey_t* keys,
                       uint32_t* vals, uint32_t* ovf, cudaStream_t st) {
     if (cap == 0) return;
     unsigned blocks = (cap + EMIT_CHUNK - 1) / EMIT_CHUNK;
+    if (AAA_K3_PERSIST) blocks = std::min(blocks, 148u * AAA_K3_MINB);
     k_cull_emit<<<blocks, EMIT_THREADS, 0, st>>>(vp, vb.cull, vb.cross, vb.offsets, n, cap, keys, vals, vb.counters,
                                                  ovf);
 }

@@ -18,8 +18,9 @@ CI = {f: i for i, f in enumerate(O.C_FIELDS)}
 MAX_VARIANTS = 4096
 
 
-def _variants(c, cfg):
-    """Yield blended (r,g,b,T) for admissible variants of the contribution list c (sorted by z)."""
+def _variants(c, cfg, tight=None):
+    """Yield blended (r,g,b,T) for admissible variants of the contribution list c (sorted by z);
+    near-tied neighbours closer than `tight` (relative, default the tie band) may swap."""
     n = c.shape[0]
     inc0 = c[:, CI["included"]] > 0.5
     flags = c[:, CI["flags"]].astype(np.int64)
@@ -30,7 +31,7 @@ def _variants(c, cfg):
     # 4e-6 relative) may swap: K6 evaluates z* in FP32 from an affine form re-centred at p_ref, whose
     # error is ~2^-24 times its condition number (|c.w_ref| + |dx c.a| + |dy c.b|) / |c.w| — up to
     # 4e-7 per depth measured on the c5 4K frame, so a 6.2e-7 gap flipped there.
-    TIGHT = cfg["band_tie"]
+    TIGHT = cfg["band_tie"] if tight is None else tight
     clusters, cur = [], [seq[0]] if seq else []
     # global-order mode (Table 5 "w/o hier. sort"): the order is the key order, exact on both sides
     pairs = zip(seq[:-1], seq[1:]) if cfg.get("order_mode", 0) == 0 else []
@@ -143,12 +144,15 @@ def _best_variant(orc, x, y, g, start, tol):
     c = orc.pixel_contribs(int(x), int(y))
     best = start
     _variants.target = np.asarray(g, dtype=np.float64)
-    for v in _variants(c, orc.cfg):
-        e = np.abs(g[:3] - v[:3]).max()
-        if e < best:
-            best = e
-        if best <= tol:
-            break
+    # two passes: swaps among depths closer than 6e-7 first (small clusters, an exhaustive search
+    # fits the variant budget), then the whole tie band (larger clusters, partly searched)
+    for tight in (min(orc.cfg["band_tie"], 6e-7), orc.cfg["band_tie"]):
+        for v in _variants(c, orc.cfg, tight):
+            e = np.abs(g[:3] - v[:3]).max()
+            if e < best:
+                best = e
+            if best <= tol:
+                return best
     return best
 
 
