@@ -15,9 +15,12 @@
 
 namespace aaa {
 
-constexpr int EMIT_THREADS = 256, EMIT_ITEMS = 8, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS, EMIT_SOFF = 4096;
+#ifndef AAA_K3_ITEMS
+#define AAA_K3_ITEMS 8
+#endif
+constexpr int EMIT_THREADS = 256, EMIT_ITEMS = AAA_K3_ITEMS, EMIT_CHUNK = EMIT_THREADS * EMIT_ITEMS, EMIT_SOFF = 4096;
 #ifndef AAA_K3_PERSIST
-#define AAA_K3_PERSIST 1
+#define AAA_K3_PERSIST 1  // A/B on c3 with the capacity-sized grid: K3 0.379 -> 0.339 ms
 #endif
 // Dense emission: every candidate c writes its (key, value) at position c, culled candidates the
 // sentinel key SKEY_NONE (above every valid key: tile ids < 2^tile_bits - 1), and the kept count
@@ -43,8 +46,10 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     __shared__ uint32_t s_off[EMIT_SOFF];
     // per-thread emitted pairs, [item][thread] (a register array indexed in a rolled loop would
     // live in local memory)
-    __shared__ skey_t s_key[EMIT_THREADS * 9];  // [t * 9 + k]: conflict-free writes, coalesced reads
-    __shared__ uint32_t s_val[EMIT_THREADS * 9];
+    // [t * (ITEMS + 1) + k] (odd stride): conflict-free writes, coalesced reads
+    constexpr int SS = EMIT_ITEMS + 1;
+    __shared__ skey_t s_key[EMIT_THREADS * SS];
+    __shared__ uint32_t s_val[EMIT_THREADS * SS];
 #if AAA_K3_PERSIST
     // persistent CTAs (a grid of resident CTAs, independent of C): each takes chunk tickets
     // until the chunks run out
@@ -182,8 +187,8 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
             keep = frustum_qp_min(cr.M, cr.muv, vp.fx, vp.fy, vp.cx, vp.cy, vp.near_z, x0, x1, y0, y1) < cr.tau;
         }
         const uint32_t tile = (uint32_t)(ty * vp.tiles_x + tx);
-        s_key[threadIdx.x * 9 + k] = keep ? ((tile << vp.key_db) | r.zkey) : SKEY_NONE;
-        s_val[threadIdx.x * 9 + k] = keep ? ((uint32_t)g | (sub << VAL_INDEX_BITS)) : 0u;
+        s_key[threadIdx.x * SS + k] = keep ? ((tile << vp.key_db) | r.zkey) : SKEY_NONE;
+        s_val[threadIdx.x * SS + k] = keep ? ((uint32_t)g | (sub << VAL_INDEX_BITS)) : 0u;
         nkeep += keep;
     }
     {
@@ -191,8 +196,8 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         const uint32_t c0 = chunk * EMIT_CHUNK;
         for (int i = threadIdx.x; i < EMIT_CHUNK; i += EMIT_THREADS) {
             if (c0 + i >= C) break;
-            keys[c0 + i] = s_key[(i >> 3) * 9 + (i & 7)];
-            vals[c0 + i] = s_val[(i >> 3) * 9 + (i & 7)];
+            keys[c0 + i] = s_key[(i / EMIT_ITEMS) * SS + i % EMIT_ITEMS];
+            vals[c0 + i] = s_val[(i / EMIT_ITEMS) * SS + i % EMIT_ITEMS];
         }
         uint32_t w = nkeep;
 #pragma unroll
