@@ -71,6 +71,14 @@ def _worker(rank, world, port, q):
         mine = full[:, 16 * a: min(16 * b, H)].clone()
         got = part.gather_bands(mine, bands, W, H, rank, world)
         ok_gather = bool(torch.equal(got, full)) if rank == 0 else got is None
+        # view gather: each rank's block of images arrives at rank 0 in rank order
+        imgs = torch.full((3, 3, 4, 5), float(rank))
+        lst = part.gather_views(imgs, rank, world)
+        if rank == 0:
+            ok_gather = ok_gather and len(lst) == world and all(torch.equal(lst[r], torch.full((3, 3, 4, 5), float(r)))
+                                                               for r in range(world))
+        else:
+            ok_gather = ok_gather and lst is None
         q.put((rank, ok_bcast, ok_gather))
     finally:
         dist.destroy_process_group()
