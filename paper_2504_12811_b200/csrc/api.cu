@@ -64,7 +64,8 @@ struct Slot {
     int deep_k = 0;
     float* d_out = nullptr;  // staging image for host outputs
     size_t d_out_cap = 0;
-    cudaEvent_t prep_done = nullptr, raster_done = nullptr;
+    cudaEvent_t prep_done = nullptr, raster_done = nullptr, k6_done = nullptr;
+    bool k6_pending = false;  // k6_done has been recorded for this slot's last view
     ViewParams vp{};
     uint32_t C = 0;
     int sorted = 0;
@@ -76,6 +77,8 @@ struct aaa_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;             // caller's stream
     cudaStream_t pstream = nullptr, rstream = nullptr;  // compute / image-copy streams
+    cudaStream_t kstream = nullptr;  // K6 stream when K1/K2 of the next view overlap K6 (overlap_k1)
+    bool overlap_k1 = true;
     cudaEvent_t ev_entry = nullptr, ev_exit = nullptr;
     aaa_config cfg{};
     aaa_camera cam{};
@@ -255,6 +258,7 @@ void free_slot(Slot& s) {
     cudaFree(s.d_out);
     if (s.prep_done) cudaEventDestroy(s.prep_done);
     if (s.raster_done) cudaEventDestroy(s.raster_done);
+    if (s.k6_done) cudaEventDestroy(s.k6_done);
     s = Slot{};
 }
 
@@ -477,6 +481,10 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     }
     const uint32_t cap = sl.pair_cap;
     const int key_bits = KEY_BITS;
+    // overlap_k1: K1/K2 of this view ran beside the previous view's K6 (K1 needs registers, K6
+    // shared memory, so they share SMs); K3 onwards need the whole GPU and wait for that K6
+    Slot& prev = ctx->slot[ctx->cur ^ 1];
+    if (ctx->overlap_k1 && prev.k6_pending) CU(cudaStreamWaitEvent(ps, prev.k6_done, 0));
     mark(3, ps);
     launch_cull_emit(vp, sl.vb, n, cap, sl.sb.keys[0], sl.sb.vals[0], ovf, ps);
     mark(4, ps);
@@ -546,24 +554,34 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         ra.rec_n = ctx->rec_n;
         ra.rec_cap = ctx->rec_cap;
     }
-    mark(10, ps);
-    launch_raster(vp, ra, ctx->cfg.window_k, ps);
-    mark(7, ps);
-    launch_raster_fallback(vp, ra, ps);
-    mark(8, ps);
+    cudaStream_t ks = ps;
+    if (ctx->overlap_k1) {
+        ks = ctx->kstream;
+        CU(cudaEventRecord(sl.prep_done, ps));
+        CU(cudaStreamWaitEvent(ks, sl.prep_done, 0));
+    }
+    mark(10, ks);
+    launch_raster(vp, ra, ctx->cfg.window_k, ks);
+    mark(7, ks);
+    launch_raster_fallback(vp, ra, ks);
+    mark(8, ks);
+    if (ctx->overlap_k1) {
+        CU(cudaEventRecord(sl.k6_done, ks));
+        sl.k6_pending = true;
+    }
     if (vp.tile_row_end > vp.tile_row_begin)  // [tile order,] K6, K6s, K6d
         ctx->launches += (ctx->cfg.flags & (AAA_FLAG_NO_3D | AAA_FLAG_NO_HIER_SORT)) ? 3 : 4;
     if (host_rgb || host_T) {
         // image D2H on the copy stream, overlapping the next view's kernels
-        CU(cudaEventRecord(sl.prep_done, ps));
+        CU(cudaEventRecord(sl.prep_done, ks));
         CU(cudaStreamWaitEvent(rs, sl.prep_done, 0));
         if (host_rgb) CU(cudaMemcpyAsync(host_rgb, ra.out_rgb, 3 * plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
         if (host_T) CU(cudaMemcpyAsync(host_T, ra.out_T, plane * sizeof(float), cudaMemcpyDeviceToHost, rs));
         mark(9, rs);
         CU(cudaEventRecord(sl.raster_done, rs));
     } else {
-        mark(9, ps);
-        CU(cudaEventRecord(sl.raster_done, ps));
+        mark(9, ks);
+        CU(cudaEventRecord(sl.raster_done, ks));
     }
     CU(cudaGetLastError());
     return AAA_OK;
@@ -575,6 +593,7 @@ aaa_status enter(aaa_ctx* ctx) {
     CU(cudaEventRecord(ctx->ev_entry, ctx->stream));
     CU(cudaStreamWaitEvent(ctx->pstream, ctx->ev_entry, 0));
     CU(cudaStreamWaitEvent(ctx->rstream, ctx->ev_entry, 0));
+    CU(cudaStreamWaitEvent(ctx->kstream, ctx->ev_entry, 0));
     return AAA_OK;
 }
 
@@ -583,6 +602,8 @@ aaa_status leave(aaa_ctx* ctx) {
     CU(cudaEventRecord(ctx->ev_exit, ctx->rstream));
     CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_exit, 0));
     CU(cudaEventRecord(ctx->ev_exit, ctx->pstream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_exit, 0));
+    CU(cudaEventRecord(ctx->ev_exit, ctx->kstream));
     CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_exit, 0));
     return AAA_OK;
 }
@@ -601,6 +622,7 @@ aaa_status unresolved_status(aaa_ctx* ctx) {
 aaa_status sync_all(aaa_ctx* ctx) {
     CU(cudaStreamSynchronize(ctx->pstream));
     CU(cudaStreamSynchronize(ctx->rstream));
+    CU(cudaStreamSynchronize(ctx->kstream));
     CU(cudaStreamSynchronize(ctx->stream));
     return AAA_OK;
 }
@@ -674,6 +696,8 @@ aaa_status render_common(aaa_ctx* ctx, const aaa_camera* cams, int n_views, int 
         // a pixel that blended more than rec_cap contributions: grow the record and render again
         const size_t npx = (size_t)W * H;
         uint32_t* d_max = ctx->rec_n + npx;  // spare word after the counts
+        CU(cudaEventRecord(ctx->ev_exit, ctx->kstream));  // the records come from K6 (kstream)
+        CU(cudaStreamWaitEvent(ctx->pstream, ctx->ev_exit, 0));
         CU(cudaMemsetAsync(d_max, 0, sizeof(uint32_t), ctx->pstream));
         launch_max_u32(ctx->rec_n, npx, d_max, ctx->pstream);
         uint32_t mx = 0;
@@ -732,11 +756,17 @@ aaa_status aaa_create(int32_t device, void* stream, aaa_ctx** out) {
     if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return bail(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->pstream, cudaStreamNonBlocking, hi)) != cudaSuccess) return bail(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->rstream, cudaStreamNonBlocking, lo)) != cudaSuccess) return bail(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->kstream, cudaStreamNonBlocking, lo)) != cudaSuccess) return bail(e);
+    {
+        const char* ov = getenv("AAA_OVERLAP_K1");
+        ctx->overlap_k1 = !(ov && ov[0] == '0');
+    }
     if ((e = cudaEventCreateWithFlags(&ctx->ev_entry, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_exit, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
     for (auto& sl : ctx->slot) {
         if ((e = cudaEventCreateWithFlags(&sl.prep_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
         if ((e = cudaEventCreateWithFlags(&sl.raster_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+        if ((e = cudaEventCreateWithFlags(&sl.k6_done, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
     }
     *out = ctx;
     return AAA_OK;
@@ -747,6 +777,7 @@ void aaa_destroy(aaa_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->pstream) cudaStreamSynchronize(ctx->pstream);
     if (ctx->rstream) cudaStreamSynchronize(ctx->rstream);
+    if (ctx->kstream) cudaStreamSynchronize(ctx->kstream);
     SceneDev& s = ctx->scene;
     cudaFree(s.geomA); cudaFree(s.geomB); cudaFree(s.geomC); cudaFree(s.sh); cudaFree(s.perm);
     for (auto& sl : ctx->slot) free_slot(sl);
@@ -761,6 +792,7 @@ void aaa_destroy(aaa_ctx* ctx) {
     if (ctx->ev_exit) cudaEventDestroy(ctx->ev_exit);
     if (ctx->pstream) cudaStreamDestroy(ctx->pstream);
     if (ctx->rstream) cudaStreamDestroy(ctx->rstream);
+    if (ctx->kstream) cudaStreamDestroy(ctx->kstream);
     delete ctx;
 }
 
