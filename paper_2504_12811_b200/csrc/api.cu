@@ -78,7 +78,7 @@ struct aaa_ctx {
     cudaStream_t stream = nullptr;             // caller's stream
     cudaStream_t pstream = nullptr, rstream = nullptr;  // compute / image-copy streams
     cudaStream_t kstream = nullptr;  // K6 stream when K1/K2 of the next view overlap K6 (overlap_k1)
-    bool overlap_k1 = true;
+    bool overlap_k1 = false;
     cudaEvent_t ev_entry = nullptr, ev_exit = nullptr;
     aaa_config cfg{};
     aaa_camera cam{};
@@ -758,8 +758,11 @@ aaa_status aaa_create(int32_t device, void* stream, aaa_ctx** out) {
     if ((e = cudaStreamCreateWithPriority(&ctx->rstream, cudaStreamNonBlocking, lo)) != cudaSuccess) return bail(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->kstream, cudaStreamNonBlocking, lo)) != cudaSuccess) return bail(e);
     {
+        // off by default: A/B on c3 258.2 -> 258.9 FPS, c2 1581 -> 1623 FPS, but K1 beside K6 slows K6
+        // by about what it hides (c3: K6 2.66 -> 3.07 ms measured with K1 inside it), which blurs
+        // the per-kernel timings the roofline figures are computed from
         const char* ov = getenv("AAA_OVERLAP_K1");
-        ctx->overlap_k1 = !(ov && ov[0] == '0');
+        ctx->overlap_k1 = ov && ov[0] == '1';
     }
     if ((e = cudaEventCreateWithFlags(&ctx->ev_entry, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_exit, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
