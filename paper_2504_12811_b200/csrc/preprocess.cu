@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 #ifndef AAA_K1_ITEMS
 #define AAA_K1_ITEMS 1
 #endif
+#ifndef AAA_K1_SPHERE
+#define AAA_K1_SPHERE 1
+#endif
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
@@ -395,8 +398,6 @@ __device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp,
 
     double mu[3] = {A4.x, A4.y, A4.z};
     double s[3] = {B4.x, B4.y, B4.z};
-    double R[9];
-    quat_to_rot(C4, R);
     double muv[3];
     mat3_vec(vp.Rv, mu, muv);
     for (int i = 0; i < 3; i++) muv[i] += vp.tv[i];
@@ -406,6 +407,27 @@ __device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp,
     double vhat = muv[2] > 0.0 ? f / muv[2] : INF;
     double veff = fmin((double)B4.w, vhat);
     double cf = isinf(veff) ? 0.0 : (double)vp.k / (veff * veff);
+#if AAA_K1_SPHERE
+    if (!DBG) {
+        // Conservative early exit (the exact whole-view cull below decides every survivor): the
+        // tau-ellipsoid lies in the sphere of radius sqrt(tau lambda_max), tau <= 2 ln(255 o) (A <= 1)
+        // and lambda_max <= max s_i^2 + k / v'^2; a sphere entirely outside one plane of the
+        // pixel-centre frustum (4 planes through the camera + z >= near) holds nothing visible.
+        // With the scene in Morton order, whole warps of off-screen Gaussians leave here.
+        const double tmax = 2.0 * log(255.0 * (double)A4.w);
+        const double lmax = fmax(fmax(s[0] * s[0], s[1] * s[1]), s[2] * s[2]) + cf;
+        const double r = sqrt(fmax(tmax, 0.0) * lmax) * (1.0 + 1e-6) + 1e-9 * fabs(muv[2]);
+        const double x0 = 0.5 - vp.cx, x1 = vp.width - 0.5 - vp.cx, y0 = 0.5 - vp.cy, y1 = vp.height - 0.5 - vp.cy;
+        const bool out = !(tmax > 0.0) || muv[2] + r < vp.near_z ||
+                         vp.fx * muv[0] - x0 * muv[2] < -r * sqrt(vp.fx * vp.fx + x0 * x0) ||
+                         -vp.fx * muv[0] + x1 * muv[2] < -r * sqrt(vp.fx * vp.fx + x1 * x1) ||
+                         vp.fy * muv[1] - y0 * muv[2] < -r * sqrt(vp.fy * vp.fy + y0 * y0) ||
+                         -vp.fy * muv[1] + y1 * muv[2] < -r * sqrt(vp.fy * vp.fy + y1 * y1);
+        if (out) return;
+    }
+#endif
+    double R[9];
+    quat_to_rot(C4, R);
     double shat[3], sig[3], isig[3];
     for (int i = 0; i < 3; i++) {
         shat[i] = s[i] * s[i] + cf;
