@@ -58,8 +58,10 @@ def main():
                                                  "deep_pixels", "unresolved_pixels", "crossing")})
         line = json.dumps(rep)
         print(line, flush=True)
-        with open(out, "a") as f:
-            f.write(line + "\n")
+        for path in (out, ROOT / "gpurun_out" / out.name):  # gpurun_out/ comes back from a GPU box
+            path.parent.mkdir(exist_ok=True)
+            with open(path, "a") as f:
+                f.write(line + "\n")
 
 
 if __name__ == "__main__":
