@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 #ifndef AAA_K1_ITEMS
 #define AAA_K1_ITEMS 1
 #endif
+// A/B (round 2, K1 ms without / with the sphere exit): c3 0.410 / 0.408, c4 inside 0.292 / 0.242,
+// c4 wide 0.454 / 0.468, c4 zoom-out 0.475 / 0.493 — kept (whole frames: c4 inside +1.2%, others
+// within 0.5%)
 #ifndef AAA_K1_SPHERE
 #define AAA_K1_SPHERE 1
 #endif
