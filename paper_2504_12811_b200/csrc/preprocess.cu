@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 // A/B (round 2, K1 ms without / with the sphere exit): c3 0.410 / 0.408, c4 inside 0.292 / 0.242,
 // c4 wide 0.454 / 0.468, c4 zoom-out 0.475 / 0.493 — kept (whole frames: c4 inside +1.2%, others
 // within 0.5%)
+#ifndef AAA_K1_SHPF
+#define AAA_K1_SHPF 2  // A/B (K1 ms, 0 / 1 L2 / 2 L1): c3 0.404 / 0.394 / 0.394, c4 wide 0.465 / 0.458 / 0.458
+#endif
 #ifndef AAA_K1_SPHERE
 #define AAA_K1_SPHERE 1
 #endif
@@ -427,6 +430,17 @@ __device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp,
                          vp.fy * muv[1] - y0 * muv[2] < -r * sqrt(vp.fy * vp.fy + y0 * y0) ||
                          -vp.fy * muv[1] + y1 * muv[2] < -r * sqrt(vp.fy * vp.fy + y1 * y1);
         if (out) return;
+    }
+#endif
+#if AAA_K1_SHPF
+    if (!DBG) {
+        // the SH coefficients are read last (colour); start their loads now so they arrive in the
+        // cache while the FP64 geometry runs (1 = L2, 2 = L1; K1 uses no shared memory)
+        const int chunks = (3 * (sc.sh_degree + 1) * (sc.sh_degree + 1) + 3) / 4;
+        for (int c = 0; c < chunks; c++) {
+            if (AAA_K1_SHPF == 2) prefetch_l1(&sc.sh[(int64_t)c * sc.n + g]);
+            else prefetch_l2(&sc.sh[(int64_t)c * sc.n + g]);
+        }
     }
 #endif
     double R[9];
