@@ -148,7 +148,8 @@ struct SortBufs {
 int sort_passes(int key_bits);
 size_t sort_state_words(uint32_t cap, int passes);
 // returns the index (0/1) of the buffer holding the sorted output
-int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st);
+int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st,
+                const uint32_t* d_kept = nullptr);
 void launch_tie_fix(const skey_t* keys, uint32_t* vals, const uint32_t* d_count, uint32_t cap, const uint32_t* perm,
                     cudaStream_t st);
 void launch_ranges(const skey_t* keys, const uint32_t* d_count, uint32_t cap, uint2* ranges, int n_tiles, int key_db,

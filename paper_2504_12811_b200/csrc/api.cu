@@ -25,6 +25,10 @@
 
 #include "aaa_internal.cuh"
 
+#ifndef AAA_SORT_DROP
+#define AAA_SORT_DROP 0  // 1: the sort's first pass drops K3's culled candidates (A/B c3: sort 0.216 either way; latency-bound passes)
+#endif
+
 using namespace aaa;
 
 cudaError_t aaa::ensure_smem_attr(const void* func, size_t bytes) {
@@ -496,7 +500,8 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         return AAA_OK;
     }
     // sort all min(C, cap) candidates (dense K3 emission: sentinels last, the first P are kept pairs)
-    int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_CCLAMP], cap, key_bits, ps);
+    int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_CCLAMP], cap, key_bits, ps,
+                             AAA_SORT_DROP ? &sl.vb.counters[CNT_P] : nullptr);
     sl.sorted = sorted;
     if (ctx->scene.perm && (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))) {
         launch_tie_fix(sl.sb.keys[sorted], sl.sb.vals[sorted], &sl.vb.counters[CNT_P], cap, ctx->scene.perm, ps);

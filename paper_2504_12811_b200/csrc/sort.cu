@@ -32,13 +32,14 @@ size_t sort_state_words(uint32_t cap, int passes) {
 }
 
 __global__ void __launch_bounds__(256) k_sort_hist(const skey_t* __restrict__ keys, const uint32_t* d_count,
-                                                    int passes, uint32_t* hist) {
+                                                    int passes, uint32_t* hist, bool drop) {
     __shared__ uint32_t sh[MAX_PASSES * 256];
     for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     uint32_t P = *d_count;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
         skey_t k = keys[i];
+        if (drop && k == SKEY_NONE) continue;
         for (int p = 0; p < passes; p++) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 0xFF)], 1u);
     }
     __syncthreads();
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
                                                            skey_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            const uint32_t* d_count, int shift,
                                                            const uint32_t* __restrict__ digit_base,
-                                                           uint32_t* state, uint32_t* ticket_ctr) {
+                                                           uint32_t* state, uint32_t* ticket_ctr, bool drop) {
     extern __shared__ __align__(16) unsigned char smem[];
     skey_t* s_keys = reinterpret_cast<skey_t*>(smem);                             // SORT_TILE
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + SORT_TILE);          // SORT_TILE
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
     uint32_t* s_bin = s_base + 256;                                              // 256 (block-local start)
     uint32_t* s_scan = s_bin + 256;                                              // 32
     uint32_t* s_ticket = s_scan + 32;
+    uint32_t* s_nvalid = s_ticket + 1;
 
     const uint32_t P = *d_count;
     if (threadIdx.x == 0) *s_ticket = atomicAdd(ticket_ctr, 1u);
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
 #pragma unroll
     for (int r = 0; r < SORT_ITEMS; r++) {
         uint64_t idx = start + w * (SORT_ITEMS * 32) + r * 32 + lane;
-        bool valid = idx < P;
+        bool valid = idx < P && !(drop && k[r] == SKEY_NONE);  // drop: culled candidates leave here
         uint32_t d = valid ? (uint32_t)((k[r] >> shift) & 0xFF) : (0x100u | lane);
         uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t prev = valid ? s_whist[w * 256 + d] : 0u;
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
         uint32_t tot;
         uint32_t bin = block_exclusive_scan(run, s_scan, &tot);
         s_bin[d] = bin;
+        if (d == 0) *s_nvalid = tot;
         // decoupled look-back for digit d over earlier tickets
         uint32_t* st = state + (size_t)b * 256 + d;
         uint32_t excl = 0;
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
 #pragma unroll
     for (int r = 0; r < SORT_ITEMS; r++) {
         uint64_t idx = start + w * (SORT_ITEMS * 32) + r * 32 + lane;
-        if (idx < P) {
+        if (idx < P && !(drop && k[r] == SKEY_NONE)) {
             uint32_t d = (uint32_t)((k[r] >> shift) & 0xFF);
             uint32_t pos = s_bin[d] + s_whist[w * 256 + d] + rank[r];
             s_keys[pos] = k[r];
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
         }
     }
     __syncthreads();
-    uint32_t nvalid = (uint32_t)min((uint64_t)SORT_TILE, (uint64_t)P - start);
+    const uint32_t nvalid = *s_nvalid;
     for (uint32_t i = threadIdx.x; i < nvalid; i += SORT_THREADS) {
         skey_t key = s_keys[i];
         uint32_t d = (uint32_t)((key >> shift) & 0xFF);
@@ -162,10 +165,14 @@ __global__ void __launch_bounds__(SORT_THREADS, AAA_SORT_MINB) k_onesweep(const 
 }
 
 static size_t onesweep_smem() {
-    return (size_t)SORT_TILE * (sizeof(skey_t) + 4) + (SORT_WARPS * 256 + 256 + 256 + 32 + 4) * 4;
+    return (size_t)SORT_TILE * (sizeof(skey_t) + 4) + (SORT_WARPS * 256 + 256 + 256 + 32 + 4 + 4) * 4;
 }
 
-int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st) {
+// d_kept != nullptr: the input holds culled candidates (key SKEY_NONE, K3's dense emission), d_kept
+// of the d_count keys are real; the first pass drops the culled ones (they would sort last) and
+// the later passes sort only the d_kept real keys.
+int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st,
+                const uint32_t* d_kept) {
     int passes = sort_passes(key_bits);
     if (cap == 0) return 0;
     unsigned blocks = (cap + SORT_TILE - 1) / SORT_TILE;
@@ -174,15 +181,16 @@ int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bit
     cudaMemsetAsync(sb.state, 0, sizeof(uint32_t) * per_pass * passes, st);
     cudaMemsetAsync(sb.tickets, 0, sizeof(uint32_t) * passes, st);
     unsigned hblocks = min(blocks, 148u * 4u);
-    k_sort_hist<<<hblocks, 256, 0, st>>>(sb.keys[0], d_count, passes, sb.hist);
+    const bool drop = d_kept != nullptr;
+    k_sort_hist<<<hblocks, 256, 0, st>>>(sb.keys[0], d_count, passes, sb.hist, drop);
     k_sort_hist_scan<<<passes, 256, 0, st>>>(sb.hist);
     if (ensure_smem_attr((const void*)k_onesweep, onesweep_smem()) != cudaSuccess) return 0;
     int cur = 0;
     for (int p = 0; p < passes; p++) {
         k_onesweep<<<blocks, SORT_THREADS, onesweep_smem(), st>>>(sb.keys[cur], sb.vals[cur], sb.keys[cur ^ 1],
-                                                                   sb.vals[cur ^ 1], d_count, 8 * p,
-                                                                   sb.hist + 256 * p, sb.state + per_pass * p,
-                                                                   sb.tickets + p);
+                                                                   sb.vals[cur ^ 1], (drop && p > 0) ? d_kept : d_count,
+                                                                   8 * p, sb.hist + 256 * p, sb.state + per_pass * p,
+                                                                   sb.tickets + p, drop && p == 0);
         cur ^= 1;
     }
     return cur;
