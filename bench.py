@@ -556,6 +556,20 @@ def bands_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n):
                "d2h_bytes_per_step": 3 * H * W * 4,
                "how": "aaa_render_band per rank + band gather + D2H of the full frame to rank 0's pinned host "
                       "buffer; wall clock, max over ranks"}
+    # outside the timed region: the gathered frame equals rank 0's own single-GPU render bit for bit
+    verify = None
+    if world > 1:
+        step()
+        frame = part.gather_bands(state["rgb"], bands, W, H, rank, world)
+        ok = torch.zeros((1,), dtype=torch.int32, device=dev)
+        if rank == 0:
+            full, _ = R.render(cam, with_T=False)
+            torch.cuda.synchronize()
+            ok[0] = int(torch.equal(frame.reshape(3, H, W), full.reshape(3, H, W)))
+        barrier(world)
+        verify = {"gathered_equals_single_gpu_frame": bool(ok.item()) if rank == 0 else None,
+                  "how": "rank 0 renders the whole frame alone (aaa_render) and compares bitwise with the "
+                         "gathered bands"}
     st = R.stats()
     stage_ms = dict(zip(STAGES, st_timed["ms"]))
     return {"metric": "frames/s (6M-Gaussian SH3 3840x2160 frame, tile-row bands)", "value": value,
@@ -566,7 +580,8 @@ def bands_mode(args, R, cams, world, rank, local, dev, stream, part, pkg, n):
                        "l2": "inputs (1.44 GB scene) larger than L2, no flush"},
             "mpix_per_s": value * W * H / 1e6, "stages_rank0": {k: stage_ms[k] for k in STAGES},
             "counters_rank0_band": {k: st[k] for k in ("visible", "candidates", "pairs", "evaluations")},
-            "gather": gather, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None}
+            "gather": gather, "verify": verify, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "cpu_baseline": None}
 
 
 def main():
