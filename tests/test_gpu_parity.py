@@ -282,6 +282,42 @@ def test_determinism_and_window_independence(R):
     assert st_deep["deep_pixels"] > 100 and st_deep["unresolved_pixels"] == 0, st_deep
 
 
+def test_exact_depth_ties_take_list_order(R):
+    """Every Gaussian twice (same geometry and opacity, different colour): each pixel sees pairs of
+    hits with exactly equal z* and alpha, whose blend order (list position, reading 4) changes the
+    colour. K6's chunk sorting network is not stable, so such chunks take the per-entry path
+    (DESIGN section 7); the image must equal the renders in which every pixel goes through K6s (order
+    field = list position) and through the 16-entry window, bit for bit, and pass the comparator
+    (exact ties are ambiguity sets)."""
+    scene, cams = S.make_config("c2")
+    sub = scene.subset(np.arange(0, scene.n, 4))
+    rng = np.random.default_rng(3)
+    sh2 = sub.sh.copy()
+    sh2[:, 0, :] = rng.uniform(-1.5, 1.5, size=(sub.n, 3)).astype(np.float32)
+    dup = S.Scene(np.concatenate([sub.means, sub.means]), np.concatenate([sub.scales, sub.scales]),
+                  np.concatenate([sub.quats, sub.quats]), np.concatenate([sub.opacities, sub.opacities]),
+                  np.concatenate([sub.sh, sh2]), np.concatenate([sub.v_train, sub.v_train]), sub.sh_degree)
+    cam = cams[7]
+    R.load(dup)
+    a = _img(R, cam)
+    R.set_config(window_k=16)
+    b = _img(R, cam)
+    R.set_config(window_k=32, flags=pkg.AAA_FLAG_FORCE_FALLBACK)
+    c = _img(R, cam)
+    R.set_config(window_k=32, flags=0)
+    assert np.array_equal(a, b), np.abs(a - b).max()
+    assert np.array_equal(a, c), np.abs(a - c).max()
+    # the ties matter: swapping the two colour sets changes the image
+    R.load(S.Scene(dup.means, dup.scales, dup.quats, dup.opacities, np.concatenate([sh2, sub.sh]), dup.v_train,
+                   dup.sh_degree))
+    d = _img(R, cam)
+    assert not np.array_equal(a, d)
+    orc = O.Oracle(dup).set_view(cam)
+    ys, xs = np.mgrid[0:cam.height:3, 0:cam.width:3]
+    rep = compare(orc, a[ys.ravel(), xs.ravel()], xs.ravel(), ys.ravel())
+    assert rep["ok"], rep
+
+
 def test_empty_scene_and_all_culled(R):
     empty = S.Scene(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32), np.zeros((0, 4), np.float32),
                     np.zeros(0, np.float32), np.zeros((0, 1, 3), np.float32), np.zeros(0, np.float32), 0)
