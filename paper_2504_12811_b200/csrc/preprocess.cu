@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(128) k_preprocess_2d(SceneDev sc, ViewParams v
 // A/B (round 2, K1 ms without / with the sphere exit): c3 0.410 / 0.408, c4 inside 0.292 / 0.242,
 // c4 wide 0.454 / 0.468, c4 zoom-out 0.475 / 0.493 — kept (whole frames: c4 inside +1.2%, others
 // within 0.5%)
+#ifndef AAA_K1_TMAX32
+#define AAA_K1_TMAX32 1  // A/B (K1 ms, FP64 / FP32 log in the sphere exit): c3 0.395 / 0.387, c4 wide 0.459 / 0.449
+#endif
 #ifndef AAA_K1_SHPF
 #define AAA_K1_SHPF 2  // A/B (K1 ms, 0 / 1 L2 / 2 L1): c3 0.404 / 0.394 / 0.394, c4 wide 0.465 / 0.458 / 0.458
 #endif
@@ -420,7 +423,12 @@ __device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp,
         // and lambda_max <= max s_i^2 + k / v'^2; a sphere entirely outside one plane of the
         // pixel-centre frustum (4 planes through the camera + z >= near) holds nothing visible.
         // With the scene in Morton order, whole warps of off-screen Gaussians leave here.
+#if AAA_K1_TMAX32
+        // an upper bound suffices here: FP32 log (a few ulp) widened by 1e-5 relative + 1e-6
+        const double tmax = (double)(2.f * __logf(255.f * A4.w)) * (1.0 + 1e-5) + 1e-6;
+#else
         const double tmax = 2.0 * log(255.0 * (double)A4.w);
+#endif
         const double lmax = fmax(fmax(s[0] * s[0], s[1] * s[1]), s[2] * s[2]) + cf;
         const double r = sqrt(fmax(tmax, 0.0) * lmax) * (1.0 + 1e-6) + 1e-9 * fabs(muv[2]);
         const double x0 = 0.5 - vp.cx, x1 = vp.width - 0.5 - vp.cx, y0 = 0.5 - vp.cy, y1 = vp.height - 0.5 - vp.cy;
