@@ -32,6 +32,9 @@ constexpr int EMIT_THREADS = 256, EMIT_ITEMS = AAA_K3_ITEMS, EMIT_CHUNK = EMIT_T
 // buffers' capacity `cap`, chunks at or beyond C exit, and a view with C > cap only processes the
 // first cap candidates and raises *ovf (the host re-renders it with larger buffers).
 
+#ifndef AAA_K3_PROBE
+#define AAA_K3_PROBE 1  // A/B (K3 ms, binary search / probes first): c3 0.339 / 0.323, c4 wide 0.334 / 0.318
+#endif
 #ifndef AAA_K3_MINB
 #define AAA_K3_MINB 3  // 80 registers, 3 CTAs of 256 threads per SM (A/B on c3: 2 -> 0.70 ms, 3 -> 0.64 ms)
 #endif
@@ -128,7 +131,17 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     for (int k = 0; k < EMIT_ITEMS; k++) {
         uint32_t c = cbeg + k;
         if (c >= C) break;
+#if AAA_K3_PROBE
+        if (g < g1 && off(g + 1) <= c) {  // next Gaussian: a few linear probes, then a binary search
+            g++;                          // (long runs of empty Gaussians: off-screen regions)
+#pragma unroll
+            for (int pr = 0; pr < 3; pr++)
+                if (g < g1 && off(g + 1) <= c) g++;
+            if (g < g1 && off(g + 1) <= c) g = find(c, g + 1);
+        }
+#else
         if (g < g1 && off(g + 1) <= c) g = find(c, g + 1);  // next Gaussian (skips empty runs)
+#endif
         if (g != g_loaded) {
             union {
                 float4 v[sizeof(CullRec) / 16];
