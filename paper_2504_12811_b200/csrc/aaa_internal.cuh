@@ -124,7 +124,8 @@ struct ViewBufs {
 constexpr int AAA_SP_CAP_LVL1 = AAA_SP_CAP;
 constexpr int CNT_VISIBLE = 0, CNT_CROSS = 1, CNT_C = 2, CNT_P = 3, CNT_SPILL = 4, CNT_SPILL_TICKET = 5,
               CNT_UNRESOLVED = 6, CNT_SCAN_TICKET = 7, CNT_SORT_TICKET = 8, CNT_EMIT_TICKET = 16, CNT_EVAL = 17,
-              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_GIANT_THR = 35, CNT_CCLAMP = 36, CNT_TOTAL = 40;
+              CNT_DEEP = 32, CNT_DEEP_TICKET = 33, CNT_GIANT = 34, CNT_GIANT_THR = 35, CNT_CCLAMP = 36, CNT_GDESC = 37,
+              CNT_GSUB = 38, CNT_GTICKET = 39, CNT_TOTAL = 40;
 
 // ---- launchers (each file implements its own) ----
 void launch_load_pack(const aaa_gaussians& in, const float* dmeans, const float* dscales, const float* dquats,
@@ -186,7 +187,19 @@ struct RasterArgs {
     float2* rec;
     uint32_t* rec_n;
     uint32_t rec_cap;
+    // giant tiles (AAA_K6_GSUB): each giant sub-tile's K6 warp writes the sub-tile's list — the
+    // list positions carrying its bit — into the sort's free ping-pong buffer (gsub, gsub_cap words)
+    // and one descriptor (tile, sub, list start, length; gdesc, tiles x 8 capacity); K6s walks the
+    // list for the sub-tile's pixels. Null gdesc: giant pixels go through the spill queue.
+    uint4* gdesc;
+    uint32_t* gsub;
+    uint32_t gsub_cap;
 };
+#ifndef AAA_K6_GSUB
+#define AAA_K6_GSUB 1  // A/B (FPS, off / on): c4 zoom-out 231.5 / 269.7, c3 301.6 / 300.1, c4 wide 256.4 / 255.6; images bit-identical
+#endif
+// gdesc[].w of a sub-tile whose list did not fit: its pixels walk the full tile list
+constexpr uint32_t GSUB_FULL = 0xFFFFFFFFu;
 void launch_raster(const ViewParams& vp, const RasterArgs& ra, int window_k, cudaStream_t st);
 
 // backward pass (backward.cu): per-Gaussian accumulators of dL/dc (3), dL/dW (9, row-major

@@ -57,6 +57,7 @@ struct Slot {
     size_t sort_state_cap = 0;
     uint2* ranges = nullptr;
     uint32_t* tile_order = nullptr;  // K6 tile launch order (longest list first)
+    uint4* gdesc = nullptr;          // giant sub-tile descriptors (tiles x 8)
     int ranges_cap = 0;
     SpillHdr* spill_hdr = nullptr;
     float4* spill_e = nullptr;
@@ -256,9 +257,9 @@ void free_slot(Slot& s) {
     ViewBufs& vb = s.vb;
     cudaFree(vb.cull); cudaFree(vb.raster); cudaFree(vb.color); cudaFree(vb.counts); cudaFree(vb.offsets);
     cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
-    for (int i = 0; i < 2; i++) { cudaFree(s.sb.keys[i]); cudaFree(s.sb.vals[i]); }
+    for (int i = 0; i < 2; i++) cudaFree(s.sb.keys[i]);  // keys and vals share one allocation
     cudaFree(s.sb.hist); cudaFree(s.sb.state); cudaFree(s.sb.tickets);
-    cudaFree(s.ranges); cudaFree(s.tile_order); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
+    cudaFree(s.ranges); cudaFree(s.tile_order); cudaFree(s.gdesc); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
     cudaFree(s.d_out);
     if (s.prep_done) cudaEventDestroy(s.prep_done);
     if (s.raster_done) cudaEventDestroy(s.raster_done);
@@ -291,10 +292,13 @@ aaa_status ensure_tiles(aaa_ctx* ctx, Slot& sl, int n_tiles) {
     if (n_tiles <= sl.ranges_cap) return AAA_OK;
     cudaFree(sl.ranges);
     cudaFree(sl.tile_order);
+    cudaFree(sl.gdesc);
     sl.ranges = nullptr;
     sl.tile_order = nullptr;
+    sl.gdesc = nullptr;
     CU(cudaMalloc(&sl.ranges, (size_t)n_tiles * sizeof(uint2)));
     CU(cudaMalloc(&sl.tile_order, (size_t)n_tiles * sizeof(uint32_t)));
+    CU(cudaMalloc(&sl.gdesc, (size_t)n_tiles * 8 * sizeof(uint4)));  // giant sub-tile descriptors
     sl.ranges_cap = n_tiles;
     return AAA_OK;
 }
@@ -341,15 +345,16 @@ aaa_status ensure_spill(aaa_ctx* ctx, Slot& sl, size_t pixels, int k) {
 aaa_status ensure_pairs(aaa_ctx* ctx, Slot& sl, uint32_t C) {
     if (C > sl.pair_cap || !sl.sb.keys[0]) {
         for (int i = 0; i < 2; i++) {
-            cudaFree(sl.sb.keys[i]);
-            cudaFree(sl.sb.vals[i]);
+            cudaFree(sl.sb.keys[i]);  // keys and vals of a ping-pong side share one allocation
             sl.sb.keys[i] = nullptr;
             sl.sb.vals[i] = nullptr;
         }
         uint32_t cap = C + C / 4 + 4096;
         for (int i = 0; i < 2; i++) {
-            CU(cudaMalloc(&sl.sb.keys[i], (size_t)cap * sizeof(skey_t)));
-            CU(cudaMalloc(&sl.sb.vals[i], (size_t)cap * sizeof(uint32_t)));
+            // one contiguous 2 x cap words per side: after the sort the free side is K6's giant
+            // sub-tile list buffer (RasterArgs::gsub)
+            CU(cudaMalloc(&sl.sb.keys[i], (size_t)cap * (sizeof(skey_t) + sizeof(uint32_t))));
+            sl.sb.vals[i] = reinterpret_cast<uint32_t*>(sl.sb.keys[i] + cap);
         }
         sl.pair_cap = cap;
         if (!sl.sb.hist) CU(cudaMalloc(&sl.sb.hist, 256 * 8 * sizeof(uint32_t)));
@@ -542,6 +547,9 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.deep_cap = (uint32_t)sl.deep_slots;
     ra.deep_k = (uint32_t)sl.deep_k;
     ra.counters = sl.vb.counters;
+    ra.gdesc = AAA_K6_GSUB ? sl.gdesc : nullptr;
+    ra.gsub = sl.sb.keys[sorted ^ 1];
+    ra.gsub_cap = 2 * cap;
     if (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) {
         const size_t npx = (size_t)cam.width * cam.height;
         if (npx * ctx->rec_cap > ctx->rec_cap_px) {
