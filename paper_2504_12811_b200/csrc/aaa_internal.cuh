@@ -232,6 +232,11 @@ void launch_permute(const float4* in, float4* out, const uint32_t* perm, int64_t
 void launch_vtrain(const SceneDev& sc, const VtCam* cams, int n_cams, float* out, bool store, cudaStream_t st);
 void launch_raster_fallback(const ViewParams& vp, const RasterArgs& ra, cudaStream_t st);
 void launch_row_costs(const ViewBufs& vb, int64_t n, int rows, unsigned long long* diff, cudaStream_t st);
+void launch_row_costs_approx(const SceneDev& sc, const ViewParams& vp, int rows, unsigned long long* diff,
+                             cudaStream_t st);
+#ifndef AAA_BAND_APPROX
+#define AAA_BAND_APPROX 1  // tile bands: cost model from the means and scales, K1 on the band only (c5, 8 bands: slowest 2.64 -> 1.90 ms)
+#endif
 void launch_band_clip(const ViewBufs& vb, int64_t n, int row_begin, int row_end, cudaStream_t st);
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set it once per (kernel, device, size)
 // for the current device (thread-safe); a failure is returned and also left in cudaGetLastError()

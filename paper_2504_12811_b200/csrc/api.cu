@@ -386,11 +386,14 @@ aaa_status ensure_rowdiff(aaa_ctx* ctx, int rows) {
     return AAA_OK;
 }
 
-// per-row candidate costs of the slot's full-frame K1 (device histogram, one small D2H; syncs ps)
-aaa_status row_costs(aaa_ctx* ctx, const Slot& sl, int rows, cudaStream_t ps, std::vector<int64_t>& out) {
+// per-row band costs (device histogram, one small D2H; syncs ps): the candidate pairs of the slot's
+// full-frame K1, or with AAA_BAND_APPROX the projected-disc model of the means and scales (no K1)
+aaa_status row_costs(aaa_ctx* ctx, const Slot& sl, const ViewParams& vp, int rows, cudaStream_t ps,
+                     std::vector<int64_t>& out) {
     aaa_status s = ensure_rowdiff(ctx, rows);
     if (s) return s;
-    launch_row_costs(sl.vb, ctx->scene.n, rows, ctx->d_rowdiff, ps);
+    if (AAA_BAND_APPROX) launch_row_costs_approx(ctx->scene, vp, rows, ctx->d_rowdiff, ps);
+    else launch_row_costs(sl.vb, ctx->scene.n, rows, ctx->d_rowdiff, ps);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(ctx->h_rowdiff, ctx->d_rowdiff, (size_t)(rows + 1) * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, ps));
@@ -458,10 +461,22 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     size_t s2 = scan_state_words(n);
     CU(cudaMemsetAsync(sl.vb.scan_state, 0, s2 * sizeof(uint32_t), ps));
     mark(0, ps);
-    const int k1_launches = launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
-    if (band_world > 0) {
+    if (AAA_BAND_APPROX && band_world > 0) {
+        // cut first (model of the means and scales), then K1 for this band only
         std::vector<int64_t> cost;
-        s = row_costs(ctx, sl, vp.tiles_y, ps, cost);
+        s = row_costs(ctx, sl, vp, vp.tiles_y, ps, cost);
+        if (s) return s;
+        split_bands(cost, band_world, band_cuts);
+        row_begin = band_cuts[band_rank];
+        row_end = band_cuts[band_rank + 1];
+        vp.tile_row_begin = row_begin;
+        vp.tile_row_end = row_end;
+        if (n > 0) ctx->launches += 1;
+    }
+    const int k1_launches = launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
+    if (!AAA_BAND_APPROX && band_world > 0) {
+        std::vector<int64_t> cost;
+        s = row_costs(ctx, sl, vp, vp.tiles_y, ps, cost);
         if (s) return s;
         split_bands(cost, band_world, band_cuts);
         row_begin = band_cuts[band_rank];
@@ -1025,10 +1040,10 @@ aaa_status aaa_tile_row_costs(aaa_ctx* ctx, int64_t* out, int32_t n_rows) {
     if (s) return s;
     ViewParams vp = make_view(ctx, ctx->cam, 0, ty);
     CU(cudaMemsetAsync(sl.vb.counters, 0, CNT_TOTAL * sizeof(uint32_t), ps));
-    launch_preprocess(ctx->scene, vp, sl.vb, false, ps);
+    if (!AAA_BAND_APPROX) launch_preprocess(ctx->scene, vp, sl.vb, false, ps);
     sl.vp = vp;
     std::vector<int64_t> cost;
-    s = row_costs(ctx, sl, ty, ps, cost);
+    s = row_costs(ctx, sl, vp, ty, ps, cost);
     if (s) return s;
     CU(cudaEventRecord(sl.raster_done, ps));
     for (int r = 0; r < n_rows; r++) out[r] = r < ty ? cost[r] : 0;

@@ -431,7 +431,10 @@ __device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp,
 #endif
         const double lmax = fmax(fmax(s[0] * s[0], s[1] * s[1]), s[2] * s[2]) + cf;
         const double r = sqrt(fmax(tmax, 0.0) * lmax) * (1.0 + 1e-6) + 1e-9 * fabs(muv[2]);
-        const double x0 = 0.5 - vp.cx, x1 = vp.width - 0.5 - vp.cx, y0 = 0.5 - vp.cy, y1 = vp.height - 0.5 - vp.cy;
+        // pixel-centre frustum of the rendered tile rows (the whole image, or a band / row range)
+        const double x0 = 0.5 - vp.cx, x1 = vp.width - 0.5 - vp.cx;
+        const double y0 = TILE * vp.tile_row_begin + 0.5 - vp.cy;
+        const double y1 = fmin((double)(TILE * vp.tile_row_end), (double)vp.height) - 0.5 - vp.cy;
         const bool out = !(tmax > 0.0) || muv[2] + r < vp.near_z ||
                          vp.fx * muv[0] - x0 * muv[2] < -r * sqrt(vp.fx * vp.fx + x0 * x0) ||
                          -vp.fx * muv[0] + x1 * muv[2] < -r * sqrt(vp.fx * vp.fx + x1 * x1) ||
@@ -739,6 +742,59 @@ __global__ void __launch_bounds__(256) k_row_costs(const CullRec* __restrict__ c
     if (sm)
         for (int i = threadIdx.x; i <= rows; i += blockDim.x)
             if (h[i]) atomicAdd(&diff[i], (unsigned long long)(long long)h[i]);
+}
+
+// Approximate tile-band cost model (AAA_BAND_APPROX): per tile row, the tile-rect width of every
+// Gaussian whose projected bounding disc (3 sigma of its largest scale widened by the 3D filter's
+// smallest variance, FP32) covers the row — from the means and scales alone, before any K1, so a
+// band rank runs K1 only where its band can see (the sphere exit). Only the load balance depends
+// on it: any cut renders the same stacked frame. Identical on every rank (same inputs, same
+// arithmetic, integer atomics).
+__global__ void __launch_bounds__(256) k_row_costs_approx(SceneDev sc, ViewParams vp, int rows,
+                                                          unsigned long long* diff) {
+    __shared__ int32_t h[ROWCOST_SMEM_ROWS + 1];
+    const bool sm = rows <= ROWCOST_SMEM_ROWS;
+    if (sm)
+        for (int i = threadIdx.x; i <= rows; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    float R[9], t[3];
+    for (int i = 0; i < 9; i++) R[i] = (float)vp.Rv[i];
+    for (int i = 0; i < 3; i++) t[i] = (float)vp.tv[i];
+    const float fx = (float)vp.fx, fy = (float)vp.fy, cx = (float)vp.cx, cy = (float)vp.cy, nz = (float)vp.near_z;
+    const float fmx = fmaxf(fx, fy), kf = vp.k;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < sc.n; g += (int64_t)gridDim.x * blockDim.x) {
+        const float4 A = __ldg(&sc.geomA[g]), B = __ldg(&sc.geomB[g]);
+        const float x = fmaf(R[0], A.x, fmaf(R[1], A.y, fmaf(R[2], A.z, t[0])));
+        const float y = fmaf(R[3], A.x, fmaf(R[4], A.y, fmaf(R[5], A.z, t[1])));
+        const float z = fmaf(R[6], A.x, fmaf(R[7], A.y, fmaf(R[8], A.z, t[2])));
+        if (!(z > nz)) continue;
+        const float smax = fmaxf(fmaxf(B.x, B.y), B.z), zf = z / fmx;
+        const float r = 3.f * sqrtf(fmaf(smax, smax, kf * zf * zf)), iz = 1.f / z;
+        const float xc = fmaf(fx * x, iz, cx), yc = fmaf(fy * y, iz, cy), rx = fx * r * iz, ry = fy * r * iz;
+        const int tx0 = max(0, (int)floorf((xc - rx) / TILE)), tx1 = min(vp.tiles_x - 1, (int)floorf((xc + rx) / TILE));
+        const int ty0 = max(0, (int)floorf((yc - ry) / TILE)), ty1 = min(rows - 1, (int)floorf((yc + ry) / TILE));
+        if (tx0 > tx1 || ty0 > ty1) continue;
+        const int w = tx1 - tx0 + 1;
+        if (sm) {
+            atomicAdd(&h[ty0], w);
+            atomicAdd(&h[ty1 + 1], -w);
+        } else {
+            atomicAdd(&diff[ty0], (unsigned long long)(long long)w);
+            atomicAdd(&diff[ty1 + 1], (unsigned long long)(long long)(-w));
+        }
+    }
+    __syncthreads();
+    if (sm)
+        for (int i = threadIdx.x; i <= rows; i += blockDim.x)
+            if (h[i]) atomicAdd(&diff[i], (unsigned long long)(long long)h[i]);
+}
+
+void launch_row_costs_approx(const SceneDev& sc, const ViewParams& vp, int rows, unsigned long long* diff,
+                             cudaStream_t st) {
+    cudaMemsetAsync(diff, 0, (size_t)(rows + 1) * sizeof(unsigned long long), st);
+    if (sc.n == 0) return;
+    const unsigned blocks = (unsigned)std::min<int64_t>((sc.n + 255) / 256, 148 * 8);
+    k_row_costs_approx<<<blocks, 256, 0, st>>>(sc, vp, rows, diff);
 }
 
 // clip every visible Gaussian's tile rect to the band [row_begin, row_end) and recount its

@@ -437,7 +437,8 @@ def test_invalid_inputs_rejected(R):
 def test_render_band_equals_full_frame(R, cfg, world):
     """aaa_render_band (SURVEY 8(e) tile bands): the bands of every rank, stacked, are the full
     frame bit for bit; the cut is the cost-balanced split of aaa_tile_row_costs (partition.band_split
-    computes the same cut on the host)."""
+    computes the same cut on the host). The cost model is the candidate pairs of a full-frame K1, or
+    (AAA_BAND_APPROX) the projected discs of the means and scales: only the balance depends on it."""
     from paper_2504_12811_b200 import partition as part
     scene, cams = S.make_config(cfg)
     cam = cams[11 if cfg == "c2" else 0]
@@ -446,7 +447,7 @@ def test_render_band_equals_full_frame(R, cfg, world):
     C_full = R.stats()["candidates"]
     R.set_camera(cam)
     costs = R.tile_row_costs()
-    assert costs.sum() == C_full
+    assert (costs >= 0).all() and 0 < costs.sum() <= 64 * C_full
     want_cuts = part.band_split(costs, world)
     rows, cuts0 = [], None
     for rank in range(world):
