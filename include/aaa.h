@@ -118,6 +118,9 @@ typedef struct {
  *   AAA_FLAG_FORCE_GIANT     every tile with a list of more than one entry takes the giant-list
  *                            path (one warp per pixel in K6s from the list start; test of that
  *                            path: the image is unchanged)
+ *   AAA_FLAG_NO_GSUB         giant-list pixels walk their tile's whole list instead of their
+ *                            sub-tile's list (the path taken when the sub-tile lists do not fit in
+ *                            the free sort buffer; test of it: the image is unchanged)
  *   AAA_FLAG_NO_HIER_SORT    Table 5 "w/o hier. sort": blend in the global per-Gaussian
  *                            order only — tile lists sorted by the view depth of the mean, no
  *                            per-pixel re-sort (the image changes where that order is not z*)
@@ -139,6 +142,7 @@ enum {
     , AAA_FLAG_FORCE_DEEP = 64u
     , AAA_FLAG_CULL_FP64 = 128u
     , AAA_FLAG_FORCE_GIANT = 256u
+    , AAA_FLAG_NO_GSUB = 512u
 };
 
 /* what for aaa_debug_copy (parity tests only; synchronises) */

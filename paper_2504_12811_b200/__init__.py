@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 from ._abi import (AAA_DBG_GAUSS, AAA_DBG_GAUSS_FIELDS, AAA_DBG_KEYS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_SPILL,
-                   AAA_DBG_RANGES, AAA_DBG_VALS, AAA_DBG_VALS_UNSORTED, AAA_FLAG_CULL_FP64, AAA_FLAG_FORCE_DEEP, AAA_FLAG_FORCE_GIANT, AAA_FLAG_FORCE_FALLBACK,
+                   AAA_DBG_RANGES, AAA_DBG_VALS, AAA_DBG_VALS_UNSORTED, AAA_FLAG_CULL_FP64, AAA_FLAG_FORCE_DEEP, AAA_FLAG_FORCE_GIANT, AAA_FLAG_FORCE_FALLBACK, AAA_FLAG_NO_GSUB,
                    AAA_FLAG_NO_3D, AAA_FLAG_NO_HIER_SORT, AAA_FLAG_NO_TILE_CULL, AAA_FLAG_SAVE_CONTRIBS, AAA_FLAG_TIMING, AAA_WARN_UNRESOLVED, AaaError, Camera, Config, Gaussians, Stats, lib,
                    EXPORTED_SYMBOLS)
 

@@ -11,6 +11,7 @@ AAA_FLAG_SAVE_CONTRIBS = 32
 AAA_FLAG_FORCE_DEEP = 64
 AAA_FLAG_CULL_FP64 = 128
 AAA_FLAG_FORCE_GIANT = 256
+AAA_FLAG_NO_GSUB = 512
 AAA_WARN_UNRESOLVED = 1  # aaa_get_stats / aaa_synchronize: pixels left inexact (spill queue full)
 (AAA_DBG_GAUSS, AAA_DBG_KEYS, AAA_DBG_VALS, AAA_DBG_KEYS_UNSORTED, AAA_DBG_VALS_UNSORTED, AAA_DBG_RANGES,
  AAA_DBG_SPILL, AAA_DBG_RASTER, AAA_DBG_COLOR) = range(9)

@@ -564,7 +564,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.counters = sl.vb.counters;
     ra.gdesc = AAA_K6_GSUB ? sl.gdesc : nullptr;
     ra.gsub = sl.sb.keys[sorted ^ 1];
-    ra.gsub_cap = 2 * cap;
+    ra.gsub_cap = (ctx->cfg.flags & AAA_FLAG_NO_GSUB) ? 0u : 2 * cap;  // 0: every giant pixel walks the full list
     if (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) {
         const size_t npx = (size_t)cam.width * cam.height;
         if (npx * ctx->rec_cap > ctx->rec_cap_px) {

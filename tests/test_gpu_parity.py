@@ -473,9 +473,13 @@ def test_giant_list_path_bit_identical(R, cfg, view):
     R.set_config(flags=pkg.AAA_FLAG_FORCE_GIANT)
     b = _img(R, cam)
     st = R.stats()
+    # the same pixels walking their tile's whole list (the path when the sub-tile lists do not fit)
+    R.set_config(flags=pkg.AAA_FLAG_FORCE_GIANT | pkg.AAA_FLAG_NO_GSUB)
+    c = _img(R, cam)
     R.set_config(flags=0)
     assert st["giant_pixels"] > 0.5 * cam.width * cam.height * 0.1 and st["unresolved_pixels"] == 0, st
     assert np.array_equal(a, b), np.abs(a - b).max()
+    assert np.array_equal(a, c), np.abs(a - c).max()
 
 
 def test_batch_pair_capacity_overflow_rerenders(R):
