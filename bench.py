@@ -352,18 +352,22 @@ def roofline_and_stages(R, views, n, deg, st_timed, abl, pkg, ms_view_wall):
             ent.update(bound="hbm", algo_bytes=sb[k], achieved_gbs=sb[k] / (t * 1e-3) / 1e9 if t else None,
                        frac_hbm=sb[k] / (t * 1e-3) / 1e9 / hbm if t else None)
         stages[k] = ent
-    traffic = None
+    traffic, ncu_k6 = None, {}
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("raster_k6")
+            tj = json.loads(tp.read_text())
+            traffic = tj.get("raster_k6")
+            ncu_k6 = {k[len("raster_k6_"):]: v for k, v in tj.items() if k.startswith("raster_k6_")}
         except Exception:
             traffic = None
     ach = stages["raster"]["achieved_tflops"]
     roof = {"kernel": "raster (K6 k_raster)", "bound": "alu", "achieved": ach, "peak": fp32, "unit": "TFLOP/s",
             "frac": ach / fp32 if ach else None, "traffic": traffic, "peak_source": fp32_src,
             "work": f"{EVAL_FLOPS} FP32 ops x {mean['evaluations']:.4g} pixel-Gaussian evaluations per view (K6)",
-            "algo_bytes_per_view": sb["raster"]}
+            "algo_bytes_per_view": sb["raster"],
+            "ncu": dict(ncu_k6, note="from the committed --set full capture (profiles/ncu_traffic.json): K6 is "
+                                     "latency-bound at 16 warps per SM (shared-memory window), not FP32-bound")}
     tot_b = sum(sb.values())
     # per-view time of one GPU from the timed loop (views overlap: K1/K2 of a view run beside the
     # previous view's K6, so the library's per-view event span is a latency, not a throughput)

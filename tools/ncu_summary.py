@@ -100,7 +100,7 @@ def main():
         d = dict(zip(hh, x))
         kern.append((base(d["Kernel Name"]), d))
     lines = [f"# {r}: ncu --set full of one c3 view (every kernel, 2nd rendered view)", "",
-             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 14 "
+             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 16 "
              "python bench.py --steps 1 --warmup 3 --scaling weak --views-per-rank 1 --no-cpu-baseline --no-e2e` (plus the pipe / bank-conflict metrics). "
              "ncu flushes caches before each replay (cold L2).", "",
              "| metric | " + " | ".join(k for k, _ in kern) + " |", "|---|" + "---|" * len(kern)]
@@ -130,6 +130,13 @@ def main():
         traffic[st] = b
     traffic["raster_k6"] = sum((float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * scale
                                for k, d in kern if k == "k_raster")
+    # K6's issue-slot utilisation and lane efficiency (it is latency-bound: the FP32 roofline
+    # fraction alone does not say how busy the SM is)
+    for k, d in kern:
+        if k == "k_raster":
+            traffic["raster_k6_issue_active"] = float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]) / 100.0
+            traffic["raster_k6_threads_per_inst"] = float(d["smsp__thread_inst_executed_per_inst_executed.ratio"])
+            traffic["raster_k6_warps_active"] = float(d["sm__warps_active.avg.pct_of_peak_sustained_active"]) / 100.0
     traffic["_source"] = f"profiles/{r}_full.md (dram__bytes_read.sum + dram__bytes_write.sum, one c3 view)"
     (PROF / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print((PROF / f"{r}_launches.md").read_text())
