@@ -1,6 +1,7 @@
 // aaa_internal.cuh — device-side layouts and launch entry points shared by the kernels of the
 // B200 forward renderer. See DESIGN.md "Data layout in HBM" for sizes.
 #pragma once
+#include <cmath>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -42,6 +43,7 @@ struct ViewParams {
     int width, height;
     int tiles_x, tiles_y;
     int tile_row_begin, tile_row_end;   // band [begin, end) of tile rows to emit
+    double fr_norm[4];  // K1 sphere exit: |normal| of the 4 pixel-centre frustum planes (set_rows)
     float k, tau_fixed, alpha_max, T_eps;
     int tau_mode;
     float bg[3];
@@ -59,6 +61,20 @@ struct ViewParams {
 };
 
 // Scene residency (L0): structure of float4 arrays, 16-byte aligned.
+// the rendered tile rows of a view and the frustum-plane norms that depend on them (K1's sphere
+// exit: sqrt(fx^2 + x0^2) etc., the same expressions K1 used to evaluate per Gaussian)
+inline void set_rows(ViewParams& vp, int row_begin, int row_end) {
+    vp.tile_row_begin = row_begin;
+    vp.tile_row_end = row_end;
+    const double x0 = 0.5 - vp.cx, x1 = vp.width - 0.5 - vp.cx;
+    const double y0 = TILE * row_begin + 0.5 - vp.cy;
+    const double y1 = std::fmin((double)(TILE * row_end), (double)vp.height) - 0.5 - vp.cy;
+    vp.fr_norm[0] = std::sqrt(vp.fx * vp.fx + x0 * x0);
+    vp.fr_norm[1] = std::sqrt(vp.fx * vp.fx + x1 * x1);
+    vp.fr_norm[2] = std::sqrt(vp.fy * vp.fy + y0 * y0);
+    vp.fr_norm[3] = std::sqrt(vp.fy * vp.fy + y1 * y1);
+}
+
 struct SceneDev {
     int64_t n;
     int sh_degree;

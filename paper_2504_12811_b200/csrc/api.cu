@@ -224,8 +224,6 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     vp.width = c.width; vp.height = c.height;
     vp.tiles_x = (c.width + TILE - 1) / TILE;
     vp.tiles_y = (c.height + TILE - 1) / TILE;
-    vp.tile_row_begin = row_begin;
-    vp.tile_row_end = row_end;
     vp.k = ctx->cfg.k;
     vp.tau_fixed = ctx->cfg.tau_fixed;
     vp.alpha_max = ctx->cfg.alpha_max;
@@ -250,6 +248,7 @@ ViewParams make_view(const aaa_ctx* ctx, const aaa_camera& c, int row_begin, int
     vp.inv_fy = 1.0 / vp.fy;
     vp.key_zmul = (1.0 - ZKEY_PAD) / vp.key_near;
     vp.giant_list = (ctx->cfg.flags & AAA_FLAG_FORCE_GIANT) ? 1u : giant_list_threshold();
+    set_rows(vp, row_begin, row_end);
     return vp;
 }
 
@@ -469,8 +468,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         split_bands(cost, band_world, band_cuts);
         row_begin = band_cuts[band_rank];
         row_end = band_cuts[band_rank + 1];
-        vp.tile_row_begin = row_begin;
-        vp.tile_row_end = row_end;
+        set_rows(vp, row_begin, row_end);
         if (n > 0) ctx->launches += 1;
     }
     const int k1_launches = launch_preprocess(ctx->scene, vp, sl.vb, debug_k1, ps);
@@ -481,8 +479,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
         split_bands(cost, band_world, band_cuts);
         row_begin = band_cuts[band_rank];
         row_end = band_cuts[band_rank + 1];
-        vp.tile_row_begin = row_begin;
-        vp.tile_row_end = row_end;
+        set_rows(vp, row_begin, row_end);
         launch_band_clip(sl.vb, n, row_begin, row_end, ps);
         if (n > 0) ctx->launches += 2;
     }

@@ -431,15 +431,16 @@ __device__ __forceinline__ void k1_one(const SceneDev& sc, const ViewParams& vp,
 #endif
         const double lmax = fmax(fmax(s[0] * s[0], s[1] * s[1]), s[2] * s[2]) + cf;
         const double r = sqrt(fmax(tmax, 0.0) * lmax) * (1.0 + 1e-6) + 1e-9 * fabs(muv[2]);
-        // pixel-centre frustum of the rendered tile rows (the whole image, or a band / row range)
+        // pixel-centre frustum of the rendered tile rows (the whole image, or a band / row range);
+        // the planes' normal lengths come with the view (set_rows)
         const double x0 = 0.5 - vp.cx, x1 = vp.width - 0.5 - vp.cx;
         const double y0 = TILE * vp.tile_row_begin + 0.5 - vp.cy;
         const double y1 = fmin((double)(TILE * vp.tile_row_end), (double)vp.height) - 0.5 - vp.cy;
         const bool out = !(tmax > 0.0) || muv[2] + r < vp.near_z ||
-                         vp.fx * muv[0] - x0 * muv[2] < -r * sqrt(vp.fx * vp.fx + x0 * x0) ||
-                         -vp.fx * muv[0] + x1 * muv[2] < -r * sqrt(vp.fx * vp.fx + x1 * x1) ||
-                         vp.fy * muv[1] - y0 * muv[2] < -r * sqrt(vp.fy * vp.fy + y0 * y0) ||
-                         -vp.fy * muv[1] + y1 * muv[2] < -r * sqrt(vp.fy * vp.fy + y1 * y1);
+                         vp.fx * muv[0] - x0 * muv[2] < -r * vp.fr_norm[0] ||
+                         -vp.fx * muv[0] + x1 * muv[2] < -r * vp.fr_norm[1] ||
+                         vp.fy * muv[1] - y0 * muv[2] < -r * vp.fr_norm[2] ||
+                         -vp.fy * muv[1] + y1 * muv[2] < -r * vp.fr_norm[3];
         if (out) return;
     }
 #endif
