@@ -98,8 +98,9 @@ def test_backward_requires_saved_render(R):
 
 def test_backward_through_spill_levels(R):
     """Blend recording through K6s and K6d (every pixel with two pending entries spills, pending
-    sets above 32 go to the deep level): the recorded blend order is the same, so the gradients
-    equal those of the default path up to atomic summation order."""
+    sets above 32 go to the deep level) and through the giant-list walks (every tile forced onto
+    it, with and without the sub-tile lists): the recorded blend order is the same, so the
+    gradients equal those of the default path up to atomic summation order."""
     scene, cams = S.make_config("c2", n=3000)
     cam = cams[7].scaled(width=128, height=128, cx=64.0, cy=64.0, fx=170.0, fy=170.0)
     rng = np.random.default_rng(4)
@@ -108,7 +109,9 @@ def test_backward_through_spill_levels(R):
     R.load(scene)
     out = {}
     try:
-        for mode, fl in (("default", 0), ("spill", pkg.AAA_FLAG_FORCE_FALLBACK | pkg.AAA_FLAG_FORCE_DEEP)):
+        for mode, fl in (("default", 0), ("spill", pkg.AAA_FLAG_FORCE_FALLBACK | pkg.AAA_FLAG_FORCE_DEEP),
+                         ("giant", pkg.AAA_FLAG_FORCE_GIANT),
+                         ("giant_full", pkg.AAA_FLAG_FORCE_GIANT | pkg.AAA_FLAG_NO_GSUB)):
             R.set_config(flags=pkg.AAA_FLAG_SAVE_CONTRIBS | fl)
             R.render(cam)
             out[mode] = {k: v.cpu().numpy() for k, v in R.backward(wr).items()}
@@ -116,7 +119,9 @@ def test_backward_through_spill_levels(R):
     finally:
         R.set_config(flags=0)
     assert out["spill_stats"]["spilled_pixels"] > 100 and out["spill_stats"]["unresolved_pixels"] == 0
-    for field in ("means", "scales", "quats", "opacities", "sh"):
-        a, b = out["default"][field], out["spill"][field]
-        # per-Gaussian sums are float atomics in pixel-thread order: compare at the field's scale
-        assert np.allclose(a, b, rtol=1e-3, atol=5e-5 * np.abs(a).max()), (field, float(np.abs(a - b).max()))
+    assert out["giant_stats"]["giant_pixels"] > 100 and out["giant_stats"]["unresolved_pixels"] == 0
+    for mode in ("spill", "giant", "giant_full"):  # also the giant-list walks (sub-tile lists / full list)
+        for field in ("means", "scales", "quats", "opacities", "sh"):
+            a, b = out["default"][field], out[mode][field]
+            # per-Gaussian sums are float atomics in pixel-thread order: compare at the field's scale
+            assert np.allclose(a, b, rtol=1e-3, atol=5e-5 * np.abs(a).max()), (mode, field, float(np.abs(a - b).max()))

@@ -462,6 +462,27 @@ def test_render_band_equals_full_frame(R, cfg, world):
     assert np.array_equal(got, full)
 
 
+def test_render_band_giant_tiles(R):
+    """Tile bands whose tiles all take the giant-list path (sub-tile lists built for the band's
+    tiles, K6s pixels written at the band's rows): stacked, the bands equal the full frame."""
+    scene, cams = S.make_config("c2")
+    cam = cams[5]
+    R.load(scene)
+    full = _img(R, cam)
+    R.set_config(flags=pkg.AAA_FLAG_FORCE_GIANT)
+    try:
+        rows = []
+        for rank in range(3):
+            rgb, T, cuts = R.render_band(rank, 3, out_T=torch.empty((cam.height * cam.width,), device="cuda:0"))
+            torch.cuda.synchronize()
+            rows.append(torch.cat([rgb, T[None]], 0).permute(1, 2, 0).cpu().numpy())
+        st = R.stats()
+    finally:
+        R.set_config(flags=0)
+    assert st["giant_pixels"] > 1000, st
+    assert np.array_equal(np.concatenate(rows, axis=0).astype(np.float64), full)
+
+
 @pytest.mark.parametrize("cfg,view", [("c2", 5), ("c4zoomout", 10)])
 def test_giant_list_path_bit_identical(R, cfg, view):
     """Tiles on the giant-list path (every pixel one K6s warp from the list start) give the same
