@@ -507,7 +507,11 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     Slot& prev = ctx->slot[ctx->cur ^ 1];
     if (ctx->overlap_k1 && prev.k6_pending) CU(cudaStreamWaitEvent(ps, prev.k6_done, 0));
     mark(3, ps);
-    launch_cull_emit(vp, sl.vb, n, cap, sl.sb.keys[0], sl.sb.vals[0], ovf, ps);
+    // AAA_K3_HIST: K3 accumulates the sort's digit histograms (zeroed here), no histogram pass
+    const bool k3_hist = AAA_K3_HIST && !AAA_SORT_DROP && stop_after == 0;
+    if (k3_hist) CU(cudaMemsetAsync(sl.sb.hist, 0, sizeof(uint32_t) * 256 * sort_passes(key_bits), ps));
+    launch_cull_emit(vp, sl.vb, n, cap, sl.sb.keys[0], sl.sb.vals[0], ovf, ps, k3_hist ? sl.sb.hist : nullptr,
+                     sort_passes(key_bits));
     mark(4, ps);
     ctx->launches += 1;
     sl.vp = vp;
@@ -518,7 +522,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     }
     // sort all min(C, cap) candidates (dense K3 emission: sentinels last, the first P are kept pairs)
     int sorted = launch_sort(sl.sb, &sl.vb.counters[CNT_CCLAMP], cap, key_bits, ps,
-                             AAA_SORT_DROP ? &sl.vb.counters[CNT_P] : nullptr);
+                             AAA_SORT_DROP ? &sl.vb.counters[CNT_P] : nullptr, k3_hist);
     sl.sorted = sorted;
     if (ctx->scene.perm && (ctx->cfg.flags & (AAA_FLAG_NO_HIER_SORT | AAA_FLAG_NO_3D))) {
         launch_tie_fix(sl.sb.keys[sorted], sl.sb.vals[sorted], &sl.vb.counters[CNT_P], cap, ctx->scene.perm, ps);
@@ -527,7 +531,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     mark(5, ps);
     launch_ranges(sl.sb.keys[sorted], &sl.vb.counters[CNT_P], cap, sl.ranges, vp.tiles_x * vp.tiles_y, vp.key_db, ps);
     mark(6, ps);
-    ctx->launches += 3 + sort_passes(key_bits);
+    ctx->launches += (k3_hist ? 2 : 3) + sort_passes(key_bits);  // [histogram,] scan, passes, ranges
     const int out_h = std::min(row_end * TILE, cam.height) - row_begin * TILE;
     const size_t plane = (size_t)out_h * cam.width;
     RasterArgs ra{};

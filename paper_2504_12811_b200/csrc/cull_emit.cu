@@ -43,8 +43,15 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
                                                             const uint32_t* __restrict__ offsets, int64_t n,
                                                             uint32_t cap, skey_t* __restrict__ keys,
                                                             uint32_t* __restrict__ vals, uint32_t* counters,
-                                                            uint32_t* ovf) {
+                                                            uint32_t* ovf, uint32_t* hist, int passes) {
     __shared__ uint32_t s_ticket, s_C;
+#if AAA_K3_HIST
+    // the sort's digit histograms of every emitted key (AAA_K3_HIST: replaces the sort's separate
+    // histogram pass), accumulated per CTA over its chunks and added to `hist` at exit
+    __shared__ uint32_t s_hist[4 * 256];
+    if (hist)
+        for (int i = threadIdx.x; i < 4 * 256; i += EMIT_THREADS) s_hist[i] = 0u;
+#endif
     __shared__ int64_t s_g0, s_g1;
     __shared__ uint32_t s_off[EMIT_SOFF];
     // per-thread emitted pairs, [item][thread] (a register array indexed in a rolled loop would
@@ -69,7 +76,14 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
     }
     __syncthreads();
     const uint32_t C = s_C;
-    if ((uint64_t)s_ticket * EMIT_CHUNK >= C) return;
+    if ((uint64_t)s_ticket * EMIT_CHUNK >= C) {
+#if AAA_K3_HIST
+        if (hist)
+            for (int i = threadIdx.x; i < passes * 256; i += EMIT_THREADS)
+                if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
+#endif
+        return;
+    }
     if (threadIdx.x < 32) {
         // the chunk's candidates [c0, c1] belong to Gaussians [g0, g1] (largest g with offset <= c):
         // two 17-ary searches side by side (half-warp each), one parallel load per step
@@ -209,8 +223,13 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
         const uint32_t c0 = chunk * EMIT_CHUNK;
         for (int i = threadIdx.x; i < EMIT_CHUNK; i += EMIT_THREADS) {
             if (c0 + i >= C) break;
-            keys[c0 + i] = s_key[(i / EMIT_ITEMS) * SS + i % EMIT_ITEMS];
+            const skey_t kk = s_key[(i / EMIT_ITEMS) * SS + i % EMIT_ITEMS];
+            keys[c0 + i] = kk;
             vals[c0 + i] = s_val[(i / EMIT_ITEMS) * SS + i % EMIT_ITEMS];
+#if AAA_K3_HIST
+            if (hist)
+                for (int p = 0; p < passes; p++) atomicAdd(&s_hist[p * 256 + ((kk >> (8 * p)) & 0xFFu)], 1u);
+#endif
         }
         uint32_t w = nkeep;
 #pragma unroll
@@ -224,12 +243,12 @@ __global__ void __launch_bounds__(EMIT_THREADS, AAA_K3_MINB) k_cull_emit(ViewPar
 }
 
 void launch_cull_emit(const ViewParams& vp, const ViewBufs& vb, int64_t n, uint32_t cap, skey_t* keys,
-                      uint32_t* vals, uint32_t* ovf, cudaStream_t st) {
+                      uint32_t* vals, uint32_t* ovf, cudaStream_t st, uint32_t* hist, int passes) {
     if (cap == 0) return;
     unsigned blocks = (cap + EMIT_CHUNK - 1) / EMIT_CHUNK;
     if (AAA_K3_PERSIST) blocks = std::min(blocks, 148u * AAA_K3_MINB);
     k_cull_emit<<<blocks, EMIT_THREADS, 0, st>>>(vp, vb.cull, vb.cross, vb.offsets, n, cap, keys, vals, vb.counters,
-                                                 ovf);
+                                                 ovf, (AAA_K3_HIST && AAA_K3_PERSIST) ? hist : nullptr, passes);
 }
 
 }  // namespace aaa

@@ -171,18 +171,19 @@ static size_t onesweep_smem() {
 // d_kept != nullptr: the input holds culled candidates (key SKEY_NONE, K3's dense emission), d_kept
 // of the d_count keys are real; the first pass drops the culled ones (they would sort last) and
 // the later passes sort only the d_kept real keys.
+// hist_ready: the digit histograms were accumulated by K3 (AAA_K3_HIST; hist zeroed before it)
 int launch_sort(SortBufs& sb, const uint32_t* d_count, uint32_t cap, int key_bits, cudaStream_t st,
-                const uint32_t* d_kept) {
+                const uint32_t* d_kept, bool hist_ready) {
     int passes = sort_passes(key_bits);
     if (cap == 0) return 0;
     unsigned blocks = (cap + SORT_TILE - 1) / SORT_TILE;
     size_t per_pass = (size_t)(blocks + 1) * 256;
-    cudaMemsetAsync(sb.hist, 0, sizeof(uint32_t) * 256 * passes, st);
+    if (!hist_ready) cudaMemsetAsync(sb.hist, 0, sizeof(uint32_t) * 256 * passes, st);
     cudaMemsetAsync(sb.state, 0, sizeof(uint32_t) * per_pass * passes, st);
     cudaMemsetAsync(sb.tickets, 0, sizeof(uint32_t) * passes, st);
     unsigned hblocks = min(blocks, 148u * 4u);
     const bool drop = d_kept != nullptr;
-    k_sort_hist<<<hblocks, 256, 0, st>>>(sb.keys[0], d_count, passes, sb.hist, drop);
+    if (!hist_ready) k_sort_hist<<<hblocks, 256, 0, st>>>(sb.keys[0], d_count, passes, sb.hist, drop);
     k_sort_hist_scan<<<passes, 256, 0, st>>>(sb.hist);
     if (ensure_smem_attr((const void*)k_onesweep, onesweep_smem()) != cudaSuccess) return 0;
     int cur = 0;
