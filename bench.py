@@ -164,8 +164,8 @@ def stage_bytes(st, n, deg, px):
         "scan": 8 * n,
         # cull record read once per visible Gaussian + its offset; (key, value) written per kept pair
         "cull_emit": (128 + 4) * V + 8 * P,
-        # histogram pass reads the keys; 4 onesweep passes read and write (key, value)
-        "sort": 4 * P + 4 * 16 * P,
+        # 4 onesweep passes read and write (key, value); the digit histograms are taken in K3
+        "sort": 4 * 16 * P,
         "ranges": 4 * P,
         # K6: (key, value) of every list entry + its 112-B raster record; RGB written per pixel
         "raster": 8 * P + 112 * P + 12 * px,
