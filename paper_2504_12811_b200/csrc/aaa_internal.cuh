@@ -212,7 +212,13 @@ struct RasterArgs {
     uint4* gdesc;
     uint32_t* gsub;
     uint32_t gsub_cap;
+    // AAA_K6S_SUBL: every tile list longer than GIANT_MIN gets sub-tile lists too; gtab[tile * 8 +
+    // sub] = (start in gsub, length or GSUB_FULL), read by K6s for the spilled pixels of those tiles
+    uint2* gtab;
 };
+#ifndef AAA_K6S_SUBL
+#define AAA_K6S_SUBL 0  // A/B (FPS, off / on): c3 306.3 / 299.7, c4 wide 264.9 / 268.5 (K6s 0.41 -> 0.32 ms), c4 inside 324.2 / 320.8
+#endif
 #ifndef AAA_K6_GSUB
 #define AAA_K6_GSUB 1  // A/B (FPS, off / on): c4 zoom-out 231.5 / 269.7, c3 301.6 / 300.1, c4 wide 256.4 / 255.6; images bit-identical
 #endif

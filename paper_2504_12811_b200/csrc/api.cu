@@ -58,6 +58,7 @@ struct Slot {
     uint2* ranges = nullptr;
     uint32_t* tile_order = nullptr;  // K6 tile launch order (longest list first)
     uint4* gdesc = nullptr;          // giant sub-tile descriptors (tiles x 8)
+    uint2* gtab = nullptr;           // sub-tile list of every long tile (tiles x 8)
     int ranges_cap = 0;
     SpillHdr* spill_hdr = nullptr;
     float4* spill_e = nullptr;
@@ -258,7 +259,7 @@ void free_slot(Slot& s) {
     cudaFree(vb.cross); cudaFree(vb.dbg); cudaFree(vb.counters); cudaFree(vb.scan_state);
     for (int i = 0; i < 2; i++) cudaFree(s.sb.keys[i]);  // keys and vals share one allocation
     cudaFree(s.sb.hist); cudaFree(s.sb.state); cudaFree(s.sb.tickets);
-    cudaFree(s.ranges); cudaFree(s.tile_order); cudaFree(s.gdesc); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
+    cudaFree(s.ranges); cudaFree(s.tile_order); cudaFree(s.gdesc); cudaFree(s.gtab); cudaFree(s.spill_hdr); cudaFree(s.spill_e); cudaFree(s.deep_hdr); cudaFree(s.deep_e);
     cudaFree(s.d_out);
     if (s.prep_done) cudaEventDestroy(s.prep_done);
     if (s.raster_done) cudaEventDestroy(s.raster_done);
@@ -292,12 +293,15 @@ aaa_status ensure_tiles(aaa_ctx* ctx, Slot& sl, int n_tiles) {
     cudaFree(sl.ranges);
     cudaFree(sl.tile_order);
     cudaFree(sl.gdesc);
+    cudaFree(sl.gtab);
     sl.ranges = nullptr;
     sl.tile_order = nullptr;
     sl.gdesc = nullptr;
+    sl.gtab = nullptr;
     CU(cudaMalloc(&sl.ranges, (size_t)n_tiles * sizeof(uint2)));
     CU(cudaMalloc(&sl.tile_order, (size_t)n_tiles * sizeof(uint32_t)));
     CU(cudaMalloc(&sl.gdesc, (size_t)n_tiles * 8 * sizeof(uint4)));  // giant sub-tile descriptors
+    CU(cudaMalloc(&sl.gtab, (size_t)n_tiles * 8 * sizeof(uint2)));   // long tiles' sub-tile lists
     sl.ranges_cap = n_tiles;
     return AAA_OK;
 }
@@ -564,6 +568,7 @@ aaa_status run_view(aaa_ctx* ctx, const aaa_camera& cam, int row_begin, int row_
     ra.deep_k = (uint32_t)sl.deep_k;
     ra.counters = sl.vb.counters;
     ra.gdesc = AAA_K6_GSUB ? sl.gdesc : nullptr;
+    ra.gtab = (AAA_K6_GSUB && AAA_K6S_SUBL) ? sl.gtab : nullptr;
     ra.gsub = sl.sb.keys[sorted ^ 1];
     ra.gsub_cap = (ctx->cfg.flags & AAA_FLAG_NO_GSUB) ? 0u : 2 * cap;  // 0: every giant pixel walks the full list
     if (ctx->cfg.flags & AAA_FLAG_SAVE_CONTRIBS) {
