@@ -99,8 +99,14 @@ def main():
     for x in data:
         d = dict(zip(hh, x))
         kern.append((base(d["Kernel Name"]), d))
+    # one view's kernels: stop where the first captured kernel comes round again (the capture
+    # window may run into the next view)
+    for i in range(1, len(kern)):
+        if kern[i][0] == kern[0][0]:
+            kern = kern[:i]
+            break
     lines = [f"# {r}: ncu --set full of one c3 view (every kernel, 2nd rendered view)", "",
-             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 16 "
+             "Command: `ncu --set full --clock-control none --import-source on -k regex:^k_ -s 15 -c 15 "
              "python bench.py --steps 1 --warmup 3 --scaling weak --views-per-rank 1 --no-cpu-baseline --no-e2e` (plus the pipe / bank-conflict metrics). "
              "ncu flushes caches before each replay (cold L2).", "",
              "| metric | " + " | ".join(k for k, _ in kern) + " |", "|---|" + "---|" * len(kern)]

@@ -17,7 +17,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     python bench.py --steps 2 --warmup 3 --scaling weak --views-per-rank 4 --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/ncu_launch_${R}.err
 tail -3 gpurun_out/ncu_launch_${R}.err
 # full capture of one whole view (the 2nd rendered view: skip the load kernel + the first view)
-timeout 1200 ncu --set full --metrics sm__inst_executed_pipe_fma.sum,sm__inst_executed_pipe_alu.sum,sm__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_lsu.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum --clock-control none --import-source on -k regex:^k_ -s 15 -c 16 \
+timeout 1200 ncu --set full --metrics sm__inst_executed_pipe_fma.sum,sm__inst_executed_pipe_alu.sum,sm__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_lsu.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum --clock-control none --import-source on -k regex:^k_ -s 15 -c 15 \
     -o gpurun_out/full_${R} -f \
     python bench.py --steps 1 --warmup 3 --scaling weak --views-per-rank 1 --no-cpu-baseline --no-e2e > /dev/null 2> gpurun_out/ncu_full_${R}.err
 tail -3 gpurun_out/ncu_full_${R}.err
